@@ -1,0 +1,1286 @@
+// ring2.cu — device Ring^2: allocator, capture kernels, publish protocol,
+// and the host consumer role. sm_100a only.
+//
+// Reference behaviour restated here (tapflow, pure Python):
+//   capture()         hooks.py:281-324   -> capture_kernel (one launch)
+//   _gather_compact   hooks.py:266-278   -> ordered compaction + 128-bit copy
+//   reserve_payload   rings.py:286-319   -> leader CTA, tf_reserve (ring2_core.h)
+//   publish           rings.py:321-353   -> last CTA: body, fence, ready_seq
+//   poll_ready        rings.py:380-406   -> tf_ring_poll_ready (host)
+//   release_payload   rings.py:408-431   -> tf_ring_release_payload (host)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <time.h>
+
+#include "ring2_internal.h"
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+void tf_set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define CUDA_TRY(expr)                                                     \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) {                                               \
+      tf_set_error("%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),        \
+                   __FILE__, __LINE__);                                    \
+      return TF_ERR_CUDA;                                                  \
+    }                                                                      \
+  } while (0)
+
+extern "C" int tf_abi_version(void) { return TF_ABI_VERSION; }
+extern "C" const char* tf_last_error(void) { return g_err.c_str(); }
+extern "C" const char* tf_status_name(int s) {
+  switch (s) {
+    case TF_OK: return "ok";
+    case TF_ERR_CONFIG: return "ConfigError";
+    case TF_ERR_ALLOCATION: return "AllocationError";
+    case TF_ERR_PAYLOAD_RING_FULL: return "PayloadRingFull";
+    case TF_ERR_META_RING_FULL: return "MetaRingFull";
+    case TF_ERR_OUT_OF_ORDER_RELEASE: return "OutOfOrderRelease";
+    case TF_ERR_PROTOCOL: return "ProtocolError";
+    case TF_ERR_META_MISMATCH: return "MetaMismatch";
+    case TF_ERR_POLICY_UNDERESTIMATE: return "PolicyUnderestimate";
+    case TF_ERR_STAGING_EXHAUSTED: return "StagingExhausted";
+    case TF_ERR_HOOK_DISABLED: return "HookDisabled";
+    case TF_ERR_VALUE: return "ValueError";
+    case TF_ERR_CUDA: return "CudaError";
+    case TF_ERR_TIMEOUT: return "Timeout";
+    case TF_ERR_EMPTY: return "Empty";
+  }
+  return "unknown";
+}
+extern "C" int tf_device_count(int* out) {
+  CUDA_TRY(cudaGetDeviceCount(out));
+  return TF_OK;
+}
+extern "C" double tf_monotonic(void) {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return double(ts.tv_sec) + 1e-9 * double(ts.tv_nsec);
+}
+
+extern "C" int tf_plan_reservation(uint64_t head, uint64_t tail, uint64_t used,
+                                   uint64_t capacity, uint64_t length,
+                                   uint64_t* offset, uint64_t* dead) {
+  uint64_t o = 0, d = 0;
+  int ok = tf_plan(head, tail, used, capacity, length, &o, &d);
+  if (offset) *offset = o;
+  if (dead) *dead = d;
+  return ok;
+}
+
+// ---------------------------------------------------------------------------
+// PTX memory-model helpers
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// streaming 128-bit loads: source activations are read exactly once
+template <int VW> struct VecT;
+template <> struct VecT<16> { using T = uint4; };
+template <> struct VecT<8> { using T = uint2; };
+template <> struct VecT<4> { using T = uint32_t; };
+template <> struct VecT<2> { using T = uint16_t; };
+template <> struct VecT<1> { using T = uint8_t; };
+
+template <int VW>
+__device__ __forceinline__ typename VecT<VW>::T ld_stream(const uint8_t* p) {
+  using T = typename VecT<VW>::T;
+  if constexpr (VW == 16) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+  } else {
+    return __ldg(reinterpret_cast<const T*>(p));
+  }
+}
+template <int VW>
+__device__ __forceinline__ void st_vec(uint8_t* p, typename VecT<VW>::T v) {
+  *reinterpret_cast<typename VecT<VW>::T*>(p) = v;
+}
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTableMax = 2048;
+constexpr int kUnroll = 8;
+constexpr int kSeg = 32 * kUnroll;  // vector words per warp segment
+constexpr int kCtasPerSm = 3;
+
+// ---------------------------------------------------------------------------
+// element conversions (bit-exact with oracle/cast_oracle.c)
+// ---------------------------------------------------------------------------
+template <int DT> struct Elem;
+template <> struct Elem<TF_F32> { static constexpr int W = 4; };
+template <> struct Elem<TF_F16> { static constexpr int W = 2; };
+template <> struct Elem<TF_BF16> { static constexpr int W = 2; };
+template <> struct Elem<TF_F8E4M3> { static constexpr int W = 1; };
+template <> struct Elem<TF_F8E5M2> { static constexpr int W = 1; };
+
+template <int DT>
+__device__ __forceinline__ float load_elem(const uint8_t* p) {
+  if constexpr (DT == TF_F32) return *reinterpret_cast<const float*>(p);
+  if constexpr (DT == TF_F16) return __half2float(*reinterpret_cast<const __half*>(p));
+  if constexpr (DT == TF_BF16) return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
+  return 0.f;
+}
+__device__ __forceinline__ float bits_to_f(int dt, uint32_t bits) {
+  if (dt == TF_F16) { __half_raw h; h.x = (unsigned short)bits; return __half2float(__half(h)); }
+  __nv_bfloat16_raw b; b.x = (unsigned short)bits; return __bfloat162float(__nv_bfloat16(b));
+}
+template <int DT>
+__device__ __forceinline__ void store_elem(uint8_t* p, float v) {
+  if constexpr (DT == TF_F32) *reinterpret_cast<float*>(p) = v;
+  if constexpr (DT == TF_F16) *reinterpret_cast<__half*>(p) = __float2half_rn(v);
+  if constexpr (DT == TF_BF16) *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+  if constexpr (DT == TF_F8E4M3) {
+    *reinterpret_cast<__nv_fp8_storage_t*>(p) =
+        __nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
+  }
+  if constexpr (DT == TF_F8E5M2) {
+    *reinterpret_cast<__nv_fp8_storage_t*>(p) =
+        __nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E5M2);
+  }
+}
+
+// 8 input elements -> 8 floats (vector path, 16/32-byte aligned)
+template <int DT>
+__device__ __forceinline__ void load8(const uint8_t* p, float* f) {
+  if constexpr (DT == TF_F32) {
+    uint4 a = ld_stream<16>(p), b = ld_stream<16>(p + 16);
+    f[0] = __uint_as_float(a.x); f[1] = __uint_as_float(a.y);
+    f[2] = __uint_as_float(a.z); f[3] = __uint_as_float(a.w);
+    f[4] = __uint_as_float(b.x); f[5] = __uint_as_float(b.y);
+    f[6] = __uint_as_float(b.z); f[7] = __uint_as_float(b.w);
+  } else {
+    uint4 a = ld_stream<16>(p);
+    uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = bits_to_f(DT, w[i] & 0xFFFFu);
+      f[2 * i + 1] = bits_to_f(DT, w[i] >> 16);
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ void store8(uint8_t* p, const float* f) {
+  if constexpr (DT == TF_F32) {
+    uint4 a = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                         __float_as_uint(f[2]), __float_as_uint(f[3]));
+    uint4 b = make_uint4(__float_as_uint(f[4]), __float_as_uint(f[5]),
+                         __float_as_uint(f[6]), __float_as_uint(f[7]));
+    *reinterpret_cast<uint4*>(p) = a;
+    *reinterpret_cast<uint4*>(p + 16) = b;
+  } else if constexpr (DT == TF_F16 || DT == TF_BF16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      unsigned short lo, hi;
+      if constexpr (DT == TF_F16) {
+        lo = __half_as_ushort(__float2half_rn(f[2 * i]));
+        hi = __half_as_ushort(__float2half_rn(f[2 * i + 1]));
+      } else {
+        lo = __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * i]));
+        hi = __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * i + 1]));
+      }
+      w[i] = uint32_t(lo) | (uint32_t(hi) << 16);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    // fp8: cvt.rn.satfinite.{e4m3,e5m2}x2.f32 packs (hi, lo)
+    uint32_t w[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      uint16_t a, b;
+      if constexpr (DT == TF_F8E4M3) {
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(a) : "f"(f[4 * i + 1]), "f"(f[4 * i]));
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(b) : "f"(f[4 * i + 3]), "f"(f[4 * i + 2]));
+      } else {
+        asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(a) : "f"(f[4 * i + 1]), "f"(f[4 * i]));
+        asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(b) : "f"(f[4 * i + 3]), "f"(f[4 * i + 2]));
+      }
+      w[i] = uint32_t(a) | (uint32_t(b) << 16);
+    }
+    *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// capture kernel
+// ---------------------------------------------------------------------------
+struct CapParams {
+  const uint8_t* src;
+  int64_t outer, mid, row_bytes, s_outer, s_mid;
+  const uint8_t* keep;
+  const uint32_t* step_ptr;
+  uint32_t step_imm, hook_id, flags, reduce_op;
+  int64_t units, rpu;         // keep units and rows per unit
+  int64_t out_row_bytes;
+  int64_t row_elems;          // elements per row (cast/reduce)
+  int64_t words_per_row;      // vector words (copy) / groups (cast) per row
+  int keep_vec;               // keep[] is 16-B aligned
+  // ring
+  uint8_t* payload;
+  uint64_t cap;
+  uint64_t slots;
+  uint8_t* meta;
+  const ConsumerShared* cons;
+  ProducerMirror* mirror;
+  tf_capture_result* result;
+  DevCtl* ctl;
+  uint64_t timeout_ns;
+};
+
+enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
+
+struct CapShared {
+  uint32_t warp_sums[kWarps];
+  uint32_t total;
+  uint32_t status;
+  uint64_t off;
+  uint32_t is_last;
+  uint32_t table[kTableMax];
+};
+
+__device__ __forceinline__ uint32_t count_nonzero_bytes(uint32_t w) {
+  uint32_t nz = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
+  return __popc(nz);
+}
+
+// Block-wide exclusive scan of one u32 per thread; returns the exclusive
+// prefix, writes the total to sh.total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, CapShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) sh.warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = lane < kWarps ? sh.warp_sums[lane] : 0u;
+    uint32_t t = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += y;
+    }
+    if (lane < kWarps) sh.warp_sums[lane] = t - s;  // exclusive warp offsets
+    if (lane == kWarps - 1) sh.total = t;
+  }
+  __syncthreads();
+  return sh.warp_sums[warp] + x - v;
+}
+
+// Leader: reservation against a fresh consumer snapshot (rings.py:286-319,
+// hooks.py:313-315: meta availability first, then payload).
+__device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows) {
+  DevCtl* c = P.ctl;
+  const uint32_t mode = P.flags & TF_FULL_MASK;
+  uint64_t len = tf_round_up16(bytes);
+  c->captures += 1;
+  uint64_t seq = ++c->capture_seq;
+  c->plan_seq = seq;
+  c->plan_bytes = bytes;
+  c->plan_rows = rows;
+  c->plan_len = len;
+  c->plan_skip = 0;
+  c->plan_kind = 0;
+  if (len > P.cap) {  // rings.py:297-298 ValueError
+    c->plan_status = TF_ERR_VALUE;
+    c->errors |= TF_DEVERR_TOO_LARGE;
+    c->drops += 1;
+    c->drop_bytes += bytes;
+    return;
+  }
+  uint64_t t0 = 0;
+  bool stalled = false;
+  for (;;) {
+    uint64_t L = ld_relaxed_sys(&P.cons->L);
+    uint64_t mtail = ld_relaxed_sys(&P.cons->meta_tail);
+    bool meta_ok = (c->meta_head - mtail) < P.slots;
+    uint32_t status = TF_ERR_META_RING_FULL;
+    if (meta_ok) {
+      tf_pstate p = c->p;
+      uint64_t off, skip;
+      uint32_t kind;
+      if (tf_reserve(&p, L, P.cap, len, &off, &skip, &kind)) {
+        c->p = p;
+        c->plan_off = off;
+        c->plan_skip = skip;
+        c->plan_kind = kind;
+        c->bytes_reserved += len;
+        if (kind & TF_DESC_DEAD_SKIP) c->dead_created += skip;
+        c->plan_status = TF_OK;
+        if (stalled) c->stall_ns += globaltimer() - t0;
+        return;
+      }
+      status = TF_ERR_PAYLOAD_RING_FULL;
+    }
+    if (mode == TF_FULL_WAIT) {
+      uint64_t now = globaltimer();
+      if (!stalled) {
+        stalled = true;
+        t0 = now;
+        c->stall_events += 1;
+      } else if (now - t0 > P.timeout_ns) {
+        c->stall_ns += now - t0;
+        c->errors |= TF_DEVERR_TIMEOUT;
+        c->drops += 1;
+        c->drop_bytes += bytes;
+        c->plan_status = TF_ERR_TIMEOUT;
+        return;
+      }
+      __nanosleep(2000);
+      continue;
+    }
+    if (mode == TF_FULL_DROP) {
+      c->drops += 1;
+      c->drop_bytes += bytes;
+      c->errors |= TF_DEVERR_UNDERESTIMATE;
+    }
+    c->plan_status = status;
+    return;
+  }
+}
+
+__device__ void write_mirror(const CapParams& P) {
+  DevCtl* c = P.ctl;
+  ProducerMirror* m = P.mirror;
+  st_relaxed_sys(&m->V, c->p.V);
+  st_relaxed_sys(&m->reset_mark, c->p.reset_mark);
+  st_relaxed_sys(&m->reset_credit, c->p.reset_credit);
+  st_relaxed_sys(&m->meta_head, c->meta_head);
+  st_relaxed_sys(&m->bytes_reserved, c->bytes_reserved);
+  st_relaxed_sys(&m->dead_created, c->dead_created);
+  st_relaxed_sys(&m->captures, c->captures);
+  st_relaxed_sys(&m->drops, c->drops);
+  st_relaxed_sys(&m->drop_bytes, c->drop_bytes);
+  st_relaxed_sys(&m->stall_events, c->stall_events);
+  st_relaxed_sys(&m->stall_ns, c->stall_ns);
+  st_relaxed_sys(&m->errors, c->errors);
+  st_relaxed_sys(&m->capture_seq, c->capture_seq);
+}
+
+// Last CTA: descriptor body, system fence, ready_seq release store
+// (rings.py:321-353; "last retiring block").
+__device__ void last_cta_publish(const CapParams& P) {
+  DevCtl* c = P.ctl;
+  tf_capture_result* res = P.result;
+  const uint32_t status = c->plan_status;
+  tf_descriptor d;
+  d.payload_offset = c->plan_off;
+  d.payload_len = c->plan_bytes;
+  d.hook_id = P.hook_id;
+  d.step_seq = P.step_ptr ? *P.step_ptr : P.step_imm;
+  d.ready_seq = TF_READY_SENTINEL;
+  d.skip_before = c->plan_skip;
+  d.flags = c->plan_kind;
+  d.n_rows = (uint32_t)c->plan_rows;
+  d.capture_seq = c->plan_seq;
+  d.reserved1 = 0;
+  if (status == TF_OK && !(P.flags & TF_CAP_DEFER_PUBLISH)) {
+    uint64_t seq = c->meta_head;
+    uint64_t slot = seq % P.slots;
+    uint64_t* w = reinterpret_cast<uint64_t*>(P.meta + slot * TF_DESCRIPTOR_SIZE);
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
+    __threadfence_system();  // payload of every CTA before the descriptor
+    st_relaxed_sys(w + 0, s[0]);
+    st_relaxed_sys(w + 1, s[1]);
+    st_relaxed_sys(w + 2, s[2]);
+    st_relaxed_sys(w + 4, s[4]);
+    st_relaxed_sys(w + 5, s[5]);
+    st_relaxed_sys(w + 6, s[6]);
+    st_relaxed_sys(w + 7, s[7]);
+    st_release_sys(w + 3, seq);  // ready_seq last
+    d.ready_seq = seq;
+    c->meta_head = seq + 1;
+  }
+  write_mirror(P);
+  // result slot
+  const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
+  uint64_t* rd = reinterpret_cast<uint64_t*>(&res->desc);
+  for (int i = 0; i < 8; ++i) st_relaxed_sys(rd + i, s[i]);
+  st_relaxed_sys(&res->payload_offset, status == TF_OK ? c->plan_off : 0);
+  st_relaxed_sys(&res->payload_len, status == TF_OK ? c->plan_bytes : 0);
+  st_relaxed_sys(&res->skip_before, c->plan_skip);
+  st_relaxed_sys(&res->ready_seq, d.ready_seq);
+  st_relaxed_sys(reinterpret_cast<uint64_t*>(&res->status),
+                 uint64_t(status) | (uint64_t(c->plan_rows) << 32));
+  st_release_sys(&res->capture_seq, c->plan_seq);
+  // re-arm the handshake for the next launch on this stream
+  c->arrive = 0;
+  c->done = 0;
+  c->plan_flag = 0;
+  __threadfence();
+}
+
+__device__ __forceinline__ const uint8_t* row_src(const CapParams& P, int64_t row) {
+  int64_t o = row / P.mid;
+  int64_t m = row - o * P.mid;
+  return P.src + o * P.s_outer + m * P.s_mid;
+}
+
+template <int MODE, int VW, int IN_DT, int OUT_DT>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams P) {
+  __shared__ CapShared sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t U = P.units;
+
+  // ---- 1. ordered compaction: count kept units, per-thread chunks ----
+  int64_t u0 = 0, u1 = 0;
+  uint32_t mycnt = 0, mybase = 0;
+  uint64_t K;
+  if (P.keep) {
+    int64_t per = (U + kThreads - 1) / kThreads;
+    if (P.keep_vec) per = (per + 15) & ~int64_t(15);
+    u0 = imin64(int64_t(tid) * per, U);
+    u1 = imin64(u0 + per, U);
+    int64_t u = u0;
+    if (P.keep_vec) {
+      for (; u + 16 <= u1; u += 16) {
+        uint4 k = *reinterpret_cast<const uint4*>(P.keep + u);
+        mycnt += count_nonzero_bytes(k.x) + count_nonzero_bytes(k.y) +
+                 count_nonzero_bytes(k.z) + count_nonzero_bytes(k.w);
+      }
+    }
+    for (; u < u1; ++u) mycnt += P.keep[u] != 0;
+    mybase = block_exclusive_scan(mycnt, sh);
+    K = sh.total;
+  } else {
+    K = (uint64_t)U;
+  }
+  const uint64_t n_rows = K * (uint64_t)P.rpu;
+  if (n_rows == 0) {  // hooks.py:309-311 nothing kept: identity, no descriptor
+    if (blockIdx.x == 0 && tid == 0) {
+      st_relaxed_sys(&P.result->payload_len, 0);
+      st_relaxed_sys(&P.result->ready_seq, TF_READY_SENTINEL);
+      st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status), TF_OK);
+      st_release_sys(&P.result->capture_seq, 0);
+    }
+    return;
+  }
+  const uint64_t out_bytes = n_rows * (uint64_t)P.out_row_bytes;
+
+  // ---- 2. reservation by the first CTA to arrive ----
+  if (tid == 0) {
+    uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
+    if (t == 0) {
+      leader_reserve(P, out_bytes, n_rows);
+      __threadfence();
+      st_release_gpu(&P.ctl->plan_flag, 1u);
+    } else {
+      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(32);
+    }
+    sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
+    sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+  }
+  __syncthreads();
+
+  if (sh.status == TF_OK) {
+    uint8_t* dst_base = P.payload + sh.off;
+    // ---- 3. this CTA's slice of the output ----
+    int64_t items, spr = 1;
+    if constexpr (MODE == MODE_REDUCE) {
+      items = (int64_t)n_rows;
+    } else {
+      spr = (P.words_per_row + kSeg - 1) / kSeg;
+      items = (int64_t)n_rows * spr;
+    }
+    const int64_t chunk = (items + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = imin64(int64_t(blockIdx.x) * chunk, items);
+    const int64_t i1 = imin64(i0 + chunk, items);
+    if (i0 < i1) {
+      const int64_t j_lo = i0 / spr, j_hi = (i1 - 1) / spr;
+      const int64_t r_lo = j_lo / P.rpu, r_hi = j_hi / P.rpu;
+      if (P.keep) {
+        // rank -> unit table for the ranks this CTA touches
+        if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
+          int64_t rank = mybase;
+          for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
+            if (P.keep[u]) {
+              if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
+              ++rank;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      auto row_of = [&](int64_t j) -> int64_t {
+        int64_t r = j / P.rpu;
+        int64_t sub = j - r * P.rpu;
+        int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
+        return unit * P.rpu + sub;
+      };
+
+      if constexpr (MODE == MODE_COPY) {
+        using V = typename VecT<VW>::T;
+        const int64_t wpr = P.words_per_row;
+        for (int64_t s = i0 + warp; s < i1; s += kWarps) {
+          const int64_t j = s / spr;
+          const int64_t k0 = (s - j * spr) * kSeg;
+          const int64_t k1 = imin64(k0 + kSeg, wpr);
+          const uint8_t* src = row_src(P, row_of(j));
+          uint8_t* dst = dst_base + j * P.out_row_bytes;
+          V v[kUnroll];
+#pragma unroll
+          for (int i = 0; i < kUnroll; ++i) {
+            int64_t k = k0 + lane + i * 32;
+            if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+          }
+#pragma unroll
+          for (int i = 0; i < kUnroll; ++i) {
+            int64_t k = k0 + lane + i * 32;
+            if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
+          }
+        }
+      } else if constexpr (MODE == MODE_CAST) {
+        // VW == 8: groups of 8 elements; VW == 1: single elements
+        constexpr int WI = Elem<IN_DT>::W, WO = Elem<OUT_DT>::W;
+        const int64_t wpr = P.words_per_row;
+        for (int64_t s = i0 + warp; s < i1; s += kWarps) {
+          const int64_t j = s / spr;
+          const int64_t k0 = (s - j * spr) * kSeg;
+          const int64_t k1 = imin64(k0 + kSeg, wpr);
+          const uint8_t* src = row_src(P, row_of(j));
+          uint8_t* dst = dst_base + j * P.out_row_bytes;
+          if constexpr (VW == 8) {
+#pragma unroll 2
+            for (int i = 0; i < kUnroll; ++i) {
+              int64_t k = k0 + lane + i * 32;
+              if (k < k1) {
+                float f[8];
+                load8<IN_DT>(src + k * 8 * WI, f);
+                store8<OUT_DT>(dst + k * 8 * WO, f);
+              }
+            }
+          } else {
+            for (int i = 0; i < kUnroll; ++i) {
+              int64_t k = k0 + lane + i * 32;
+              if (k < k1) store_elem<OUT_DT>(dst + k * WO, load_elem<IN_DT>(src + k * WI));
+            }
+          }
+        }
+      } else {
+        // MODE_REDUCE: one warp per row, fp64 accumulation, f32 outputs
+        constexpr int WI = Elem<IN_DT>::W;
+        const int64_t H = P.row_elems;
+        for (int64_t j = i0 + warp; j < i1; j += kWarps) {
+          const uint8_t* src = row_src(P, row_of(j));
+          double sum = 0.0, sq = 0.0;
+          float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
+          if (VW == 8) {
+            const int64_t G8 = H / 8;
+            for (int64_t g = lane; g < G8; g += 32) {
+              float f[8];
+              load8<IN_DT>(src + g * 8 * WI, f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                sum += (double)f[e];
+                sq += (double)f[e] * (double)f[e];
+                mn = fminf(mn, f[e]);
+                mx = fmaxf(mx, f[e]);
+                amax = fmaxf(amax, fabsf(f[e]));
+              }
+            }
+          } else {
+            for (int64_t e = lane; e < H; e += 32) {
+              float x = load_elem<IN_DT>(src + e * WI);
+              sum += (double)x;
+              sq += (double)x * (double)x;
+              mn = fminf(mn, x);
+              mx = fmaxf(mx, x);
+              amax = fmaxf(amax, fabsf(x));
+            }
+          }
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            sq += __shfl_xor_sync(0xffffffffu, sq, d);
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, d));
+          }
+          if (lane == 0) {
+            float* o = reinterpret_cast<float*>(dst_base + j * P.out_row_bytes);
+            switch (P.reduce_op) {
+              case TF_RED_MEAN: o[0] = (float)(sum / (double)H); break;
+              case TF_RED_L2: o[0] = (float)sqrt(sq); break;
+              case TF_RED_ABSMAX: o[0] = amax; break;
+              case TF_RED_RMS: o[0] = (float)sqrt(sq / (double)H); break;
+              default:
+                o[0] = (float)(sum / (double)H);
+                o[1] = (float)sqrt(sq);
+                o[2] = mn;
+                o[3] = mx;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  // ---- 4. last CTA publishes ----
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    uint32_t t = atomicAdd(&P.ctl->done, 1u);
+    sh.is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (sh.is_last && tid == 0) {
+    __threadfence();
+    last_cta_publish(P);
+  }
+}
+
+// Protocol-level producer ops (single thread): the same allocator and
+// publish rules exposed one call at a time, for the reference's ring tests.
+__global__ void reserve_kernel(CapParams P, uint64_t len) {
+  DevCtl* c = P.ctl;
+  uint64_t L = ld_relaxed_sys(&P.cons->L);
+  tf_pstate p = c->p;
+  uint64_t off = 0, skip = 0;
+  uint32_t kind = 0;
+  uint32_t status = TF_ERR_PAYLOAD_RING_FULL;
+  if (tf_reserve(&p, L, P.cap, len, &off, &skip, &kind)) {
+    c->p = p;
+    c->bytes_reserved += len;
+    if (kind & TF_DESC_DEAD_SKIP) c->dead_created += skip;
+    status = TF_OK;
+  }
+  write_mirror(P);
+  st_relaxed_sys(&P.result->payload_offset, off);
+  st_relaxed_sys(&P.result->skip_before, skip);
+  st_relaxed_sys(&P.result->payload_len, len);
+  st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status),
+                 uint64_t(status) | (uint64_t(kind) << 32));
+  __threadfence_system();
+}
+
+__global__ void publish_kernel(CapParams P, tf_descriptor d) {
+  DevCtl* c = P.ctl;
+  uint64_t mtail = ld_relaxed_sys(&P.cons->meta_tail);
+  uint32_t status = TF_OK;
+  uint64_t seq = TF_READY_SENTINEL;
+  if (c->meta_head - mtail >= P.slots) {
+    status = TF_ERR_META_RING_FULL;  // rings.py:327-330
+  } else {
+    uint64_t slot = c->meta_head % P.slots;
+    uint64_t* w = reinterpret_cast<uint64_t*>(P.meta + slot * TF_DESCRIPTOR_SIZE);
+    if (ld_relaxed_sys(w + 3) != TF_READY_SENTINEL) {
+      status = TF_ERR_PROTOCOL;  // rings.py:334-335
+      c->errors |= TF_DEVERR_PROTOCOL;
+    } else {
+      seq = c->meta_head;
+      d.ready_seq = TF_READY_SENTINEL;
+      const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
+      __threadfence_system();
+      for (int i = 0; i < 8; ++i)
+        if (i != 3) st_relaxed_sys(w + i, s[i]);
+      st_release_sys(w + 3, seq);
+      c->meta_head = seq + 1;
+    }
+  }
+  write_mirror(P);
+  st_relaxed_sys(&P.result->ready_seq, seq);
+  st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status), status);
+  __threadfence_system();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host: ring lifecycle
+// ---------------------------------------------------------------------------
+static int set_device(int dev) {
+  CUDA_TRY(cudaSetDevice(dev));
+  return TF_OK;
+}
+
+static CapParams base_params(tf_ring* r) {
+  CapParams P;
+  memset(&P, 0, sizeof(P));
+  P.payload = r->payload;
+  P.cap = r->cfg.payload_capacity;
+  P.slots = r->cfg.meta_slots;
+  P.meta = r->meta;
+  P.cons = r->cons;
+  P.mirror = r->mirror;
+  P.result = r->result;
+  P.ctl = r->ctl;
+  P.timeout_ns = r->cfg.wait_timeout_ns ? r->cfg.wait_timeout_ns : 30000000000ull;
+  return P;
+}
+
+extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** out) {
+  if (!cfg || !out) { tf_set_error("null argument"); return TF_ERR_VALUE; }
+  // rings.py:75-85 RingConfig validation
+  if (cfg->payload_capacity == 0) { tf_set_error("payload_capacity must be positive"); return TF_ERR_CONFIG; }
+  if (cfg->payload_capacity % TF_COPY_UNIT) {
+    tf_set_error("payload_capacity must be a multiple of 16 bytes");
+    return TF_ERR_CONFIG;
+  }
+  if (cfg->meta_slots == 0) { tf_set_error("meta_slots must be positive"); return TF_ERR_CONFIG; }
+  if (!(cfg->high_watermark > 0.0 && cfg->high_watermark <= 1.0)) {
+    tf_set_error("high_watermark must be in (0, 1]");
+    return TF_ERR_CONFIG;
+  }
+  int rc = set_device(device);
+  if (rc) return rc;
+  tf_ring* r = new tf_ring();
+  r->device = device;
+  r->cfg = *cfg;
+  auto fail = [&](int code) {
+    if (r->payload) cudaFree(r->payload);
+    if (r->ctl) cudaFree(r->ctl);
+    if (r->meta) cudaFreeHost(r->meta);
+    if (r->cons) cudaFreeHost(r->cons);
+    if (r->mirror) cudaFreeHost(r->mirror);
+    if (r->result) cudaFreeHost(r->result);
+    delete r;
+    return code;
+  };
+  cudaError_t e = cudaMalloc(&r->payload, cfg->payload_capacity);
+  if (e != cudaSuccess) {
+    tf_set_error("device arena cannot satisfy %llu bytes: %s",
+                 (unsigned long long)cfg->payload_capacity, cudaGetErrorString(e));
+    cudaGetLastError();
+    return fail(TF_ERR_ALLOCATION);  // rings.py:155-160 AllocationError
+  }
+  const unsigned hflags = cudaHostAllocMapped | cudaHostAllocPortable;
+  size_t meta_bytes = size_t(cfg->meta_slots) * TF_DESCRIPTOR_SIZE;
+  if (cudaHostAlloc((void**)&r->meta, meta_bytes, hflags) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->cons, sizeof(ConsumerShared), hflags) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->mirror, sizeof(ProducerMirror), hflags) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->result, sizeof(tf_capture_result), hflags) != cudaSuccess) {
+    tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(TF_ERR_ALLOCATION);
+  }
+  memset(r->meta, 0, meta_bytes);
+  for (uint32_t s = 0; s < cfg->meta_slots; ++s)  // rings.py:213-215
+    reinterpret_cast<uint64_t*>(r->meta + size_t(s) * TF_DESCRIPTOR_SIZE)[3] = TF_READY_SENTINEL;
+  memset(r->cons, 0, sizeof(ConsumerShared));
+  memset(r->mirror, 0, sizeof(ProducerMirror));
+  r->mirror->reset_mark = TF_NO_MARK;
+  memset(r->result, 0, sizeof(tf_capture_result));
+  if (cudaMalloc(&r->ctl, sizeof(DevCtl)) != cudaSuccess) {
+    tf_set_error("device control block allocation failed");
+    cudaGetLastError();
+    return fail(TF_ERR_ALLOCATION);
+  }
+  DevCtl init;
+  memset(&init, 0, sizeof(init));
+  init.p.reset_mark = TF_NO_MARK;
+  if (cudaMemcpy(r->ctl, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(r->payload, 0, cfg->payload_capacity) != cudaSuccess) {
+    tf_set_error("device init failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(TF_ERR_CUDA);
+  }
+  cudaStream_t s;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    tf_set_error("stream create failed");
+    return fail(TF_ERR_CUDA);
+  }
+  r->own_stream = s;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(TF_ERR_CUDA);
+  *out = r;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_destroy(tf_ring* r) {
+  if (!r) return TF_OK;
+  cudaSetDevice(r->device);
+  cudaDeviceSynchronize();
+  if (r->own_stream) cudaStreamDestroy((cudaStream_t)r->own_stream);
+  cudaFree(r->payload);
+  cudaFree(r->ctl);
+  cudaFreeHost(r->meta);
+  cudaFreeHost(r->cons);
+  cudaFreeHost(r->mirror);
+  cudaFreeHost(r->result);
+  delete r;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_payload_ptr(tf_ring* r, void** p) {
+  if (!r || !p) return TF_ERR_VALUE;
+  *p = r->payload;
+  return TF_OK;
+}
+extern "C" int tf_ring_meta_ptr(tf_ring* r, void** p) {
+  if (!r || !p) return TF_ERR_VALUE;
+  *p = r->meta;
+  return TF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host: capture launch
+// ---------------------------------------------------------------------------
+static int dtype_width(uint32_t dt) {
+  switch (dt) {
+    case TF_U8: case TF_I8: case TF_F8E4M3: case TF_F8E5M2: return 1;
+    case TF_F16: case TF_BF16: return 2;
+    case TF_F32: case TF_I32: return 4;
+    case TF_F64: case TF_I64: return 8;
+  }
+  return 0;
+}
+static int reduce_k(uint32_t op) { return op == TF_RED_STATS ? 4 : 1; }
+
+extern "C" int tf_capture_out_row_bytes(const tf_capture_args* a, int64_t* out) {
+  if (!a || !out) return TF_ERR_VALUE;
+  if (a->op == TF_OP_COPY) { *out = a->row_bytes; return TF_OK; }
+  int wi = dtype_width(a->in_dtype);
+  if (wi == 0 || a->row_bytes % wi) { tf_set_error("row_bytes not a multiple of the input width"); return TF_ERR_CONFIG; }
+  int64_t elems = a->row_bytes / wi;
+  if (a->op == TF_OP_CAST) {
+    int wo = dtype_width(a->out_dtype);
+    if (!wo) { tf_set_error("bad out dtype"); return TF_ERR_CONFIG; }
+    *out = elems * wo;
+    return TF_OK;
+  }
+  if (a->op == TF_OP_REDUCE) {
+    if (a->reduce_op > TF_RED_STATS) { tf_set_error("bad reduce op"); return TF_ERR_CONFIG; }
+    *out = int64_t(reduce_k(a->reduce_op)) * 4;
+    return TF_OK;
+  }
+  tf_set_error("bad op");
+  return TF_ERR_CONFIG;
+}
+
+template <int MODE, int VW, int IN, int OUT>
+static int launch(const CapParams& P, int grid, cudaStream_t s) {
+  capture_kernel<MODE, VW, IN, OUT><<<grid, kThreads, 0, s>>>(P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    tf_set_error("capture launch: %s", cudaGetErrorString(e));
+    return TF_ERR_CUDA;
+  }
+  return TF_OK;
+}
+
+static int pow2_align(uint64_t x) {
+  if (x == 0) return 16;
+  int a = 1;
+  while (a < 16 && (x % (uint64_t)(a * 2)) == 0) a *= 2;
+  return a;
+}
+
+template <int IN, int OUT>
+static int launch_cast(const CapParams& P, bool vec, int grid, cudaStream_t s) {
+  return vec ? launch<MODE_CAST, 8, IN, OUT>(P, grid, s) : launch<MODE_CAST, 1, IN, OUT>(P, grid, s);
+}
+template <int IN>
+static int launch_cast_in(const CapParams& P, uint32_t out, bool vec, int grid, cudaStream_t s) {
+  switch (out) {
+    case TF_F32: return launch_cast<IN, TF_F32>(P, vec, grid, s);
+    case TF_F16: return launch_cast<IN, TF_F16>(P, vec, grid, s);
+    case TF_BF16: return launch_cast<IN, TF_BF16>(P, vec, grid, s);
+    case TF_F8E4M3: return launch_cast<IN, TF_F8E4M3>(P, vec, grid, s);
+    case TF_F8E5M2: return launch_cast<IN, TF_F8E5M2>(P, vec, grid, s);
+  }
+  tf_set_error("cast output dtype %u unsupported", out);
+  return TF_ERR_CONFIG;
+}
+template <int IN>
+static int launch_reduce(const CapParams& P, bool vec, int grid, cudaStream_t s) {
+  return vec ? launch<MODE_REDUCE, 8, IN, TF_F32>(P, grid, s)
+             : launch<MODE_REDUCE, 1, IN, TF_F32>(P, grid, s);
+}
+
+static int g_sm_count = 0;
+
+extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
+  if (!r || !a) { tf_set_error("null argument"); return TF_ERR_VALUE; }
+  // TensorView validation, hooks.py:209-217
+  if (a->outer <= 0 || a->mid <= 0 || a->row_bytes <= 0) {
+    tf_set_error("view shape must be non-empty and positive");
+    return TF_ERR_CONFIG;
+  }
+  if (!a->src) { tf_set_error("null source"); return TF_ERR_VALUE; }
+  int64_t orb;
+  int rc = tf_capture_out_row_bytes(a, &orb);
+  if (rc) return rc;
+  int rcd = set_device(r->device);
+  if (rcd) return rcd;
+  if (!g_sm_count) {
+    int dev = r->device, n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count = n;
+  }
+  CapParams P = base_params(r);
+  P.src = (const uint8_t*)a->src;
+  P.outer = a->outer;
+  P.mid = a->mid;
+  P.row_bytes = a->row_bytes;
+  P.s_outer = a->stride_outer;
+  P.s_mid = a->stride_mid;
+  P.keep = a->keep;
+  P.step_ptr = a->step_seq_ptr;
+  P.step_imm = a->step_seq;
+  P.hook_id = a->hook_id;
+  P.flags = a->flags;
+  P.reduce_op = a->reduce_op;
+  const bool per_outer = (a->flags & TF_CAP_KEEP_PER_OUTER) != 0;
+  P.units = per_outer ? a->outer : a->outer * a->mid;
+  P.rpu = per_outer ? a->mid : 1;
+  P.out_row_bytes = orb;
+  P.keep_vec = ((uintptr_t)a->keep % 16) == 0;
+  if ((a->flags & TF_FULL_MASK) > TF_FULL_DROP) { tf_set_error("bad full mode"); return TF_ERR_CONFIG; }
+
+  // alignment every source row start shares (pow2, capped at 16)
+  int sal = pow2_align((uintptr_t)a->src);
+  if (a->outer > 1) sal = std::min(sal, pow2_align((uint64_t)a->stride_outer));
+  if (a->mid > 1) sal = std::min(sal, pow2_align((uint64_t)a->stride_mid));
+  const int64_t total_rows = a->outer * a->mid;
+  const uint64_t out_max = uint64_t(total_rows) * uint64_t(orb);
+  int grid_bytes = int(std::min<uint64_t>((out_max + (16u << 10) - 1) / (16u << 10),
+                                          uint64_t(g_sm_count) * kCtasPerSm));
+  int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
+  int grid = std::max(1, std::max(grid_bytes, grid_table));
+  if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));
+  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+
+  if (a->op == TF_OP_COPY) {
+    int vw = std::min<int>(sal, pow2_align((uint64_t)a->row_bytes));
+    P.words_per_row = a->row_bytes / vw;
+    switch (vw) {
+      case 16: return launch<MODE_COPY, 16, 0, 0>(P, grid, s);
+      case 8: return launch<MODE_COPY, 8, 0, 0>(P, grid, s);
+      case 4: return launch<MODE_COPY, 4, 0, 0>(P, grid, s);
+      case 2: return launch<MODE_COPY, 2, 0, 0>(P, grid, s);
+      default: return launch<MODE_COPY, 1, 0, 0>(P, grid, s);
+    }
+  }
+  const int wi = dtype_width(a->in_dtype);
+  P.row_elems = a->row_bytes / wi;
+  if (a->in_dtype != TF_F32 && a->in_dtype != TF_F16 && a->in_dtype != TF_BF16) {
+    tf_set_error("cast/reduce input dtype must be f32, f16 or bf16");
+    return TF_ERR_CONFIG;
+  }
+  // 8-element groups need 16-B aligned input groups
+  const bool vec = (P.row_elems % 8 == 0) && sal >= 16 && ((uint64_t)(8 * wi) % 16 == 0);
+  if (a->op == TF_OP_CAST) {
+    P.words_per_row = vec ? P.row_elems / 8 : P.row_elems;
+    switch (a->in_dtype) {
+      case TF_F32: return launch_cast_in<TF_F32>(P, a->out_dtype, vec, grid, s);
+      case TF_F16: return launch_cast_in<TF_F16>(P, a->out_dtype, vec, grid, s);
+      default: return launch_cast_in<TF_BF16>(P, a->out_dtype, vec, grid, s);
+    }
+  }
+  P.words_per_row = 1;
+  // reduce: one warp per row; size the grid by rows
+  {
+    int64_t g = (total_rows + kWarps - 1) / kWarps;
+    int gr = int(std::min<int64_t>(g, int64_t(g_sm_count) * kCtasPerSm));
+    grid = std::max(std::max(gr, grid_table), 1);
+  }
+  switch (a->in_dtype) {
+    case TF_F32: return launch_reduce<TF_F32>(P, vec, grid, s);
+    case TF_F16: return launch_reduce<TF_F16>(P, vec, grid, s);
+    default: return launch_reduce<TF_BF16>(P, vec, grid, s);
+  }
+}
+
+extern "C" int tf_ring_last_result(tf_ring* r, tf_capture_result* out) {
+  if (!r || !out) return TF_ERR_VALUE;
+  memcpy(out, (const void*)r->result, sizeof(*out));
+  out->status = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) & 0xFFFFFFFFu);
+  out->n_rows = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) >> 32);
+  return TF_OK;
+}
+
+extern "C" int tf_ring_reserve(tf_ring* r, void* stream, uint64_t length,
+                               uint64_t* offset, uint64_t* skip_before) {
+  if (!r) return TF_ERR_VALUE;
+  // rings.py:293-298
+  if (length == 0) { tf_set_error("reservation length must be positive"); return TF_ERR_VALUE; }
+  if (length % TF_COPY_UNIT) { tf_set_error("reservation length must be a copy-unit multiple"); return TF_ERR_VALUE; }
+  if (length > r->cfg.payload_capacity) { tf_set_error("reservation exceeds payload capacity"); return TF_ERR_VALUE; }
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+  CapParams P = base_params(r);
+  reserve_kernel<<<1, 1, 0, s>>>(P, length);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s));
+  uint64_t st = *reinterpret_cast<volatile uint64_t*>(&r->result->status);
+  uint32_t status = uint32_t(st & 0xFFFFFFFFu), kind = uint32_t(st >> 32);
+  if (status != TF_OK) {
+    tf_set_error("need %llu bytes", (unsigned long long)length);
+    return TF_ERR_PAYLOAD_RING_FULL;
+  }
+  uint64_t off = r->result->payload_offset, skip = r->result->skip_before;
+  {
+    std::lock_guard<std::mutex> g(r->mu);
+    HostRegion hr{off, length, skip, kind};
+    r->regions.push_back(hr);
+    r->host_reserved[off] = hr;
+  }
+  if (offset) *offset = off;
+  if (skip_before) *skip_before = skip;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_publish(tf_ring* r, void* stream, const tf_descriptor* d,
+                               uint64_t* ready_seq) {
+  if (!r || !d) return TF_ERR_VALUE;
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+  tf_descriptor dd = *d;
+  if (dd.capture_seq == 0) {
+    // user-built descriptor for a tf_ring_reserve'd region: its region is
+    // already in the host FIFO; carry the skip for completeness.
+    std::lock_guard<std::mutex> g(r->mu);
+    auto it = r->host_reserved.find(dd.payload_offset);
+    if (it != r->host_reserved.end()) {
+      dd.skip_before = it->second.skip;
+      dd.flags = it->second.kind;
+    }
+    dd.flags |= TF_DESC_HOST_RESERVED;
+  }
+  CapParams P = base_params(r);
+  publish_kernel<<<1, 1, 0, s>>>(P, dd);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s));
+  uint32_t status = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) & 0xFFFFFFFFu);
+  if (status == TF_ERR_META_RING_FULL) {
+    tf_set_error("all %u descriptor slots are in flight", r->cfg.meta_slots);
+    return status;
+  }
+  if (status == TF_ERR_PROTOCOL) {
+    tf_set_error("descriptor slot reused before consumption");
+    return status;
+  }
+  if (dd.capture_seq == 0) {
+    std::lock_guard<std::mutex> g(r->mu);
+    r->host_reserved.erase(dd.payload_offset);
+  }
+  if (ready_seq) *ready_seq = r->result->ready_seq;
+  return TF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host: consumer role
+// ---------------------------------------------------------------------------
+static inline uint64_t slot_ready(const tf_ring* r, uint64_t slot) {
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE) + 3;
+  return __atomic_load_n(p, __ATOMIC_ACQUIRE);
+}
+
+int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
+                     uint32_t* n, bool consume) {
+  uint32_t got = 0;
+  const uint64_t slots = r->cfg.meta_slots;
+  uint64_t tail = r->meta_tail;
+  while (got < max_entries && got < slots) {
+    uint64_t slot = tail % slots;
+    uint64_t ready = slot_ready(r, slot);
+    if (ready == TF_READY_SENTINEL) break;
+    tf_descriptor d;
+    memcpy(&d, r->meta + slot * TF_DESCRIPTOR_SIZE, sizeof(d));
+    d.ready_seq = ready;
+    if (consume) {
+      if (ready != r->consumed) {  // rings.py:397-401
+        tf_set_error("descriptor sequence %llu out of order, expected %llu",
+                     (unsigned long long)ready, (unsigned long long)r->consumed);
+        *n = got;
+        return TF_ERR_PROTOCOL;
+      }
+      uint64_t* rp = reinterpret_cast<uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE) + 3;
+      __atomic_store_n(rp, TF_READY_SENTINEL, __ATOMIC_RELEASE);
+      r->meta_tail = ++tail;
+      r->consumed += 1;
+      __atomic_store_n(&r->cons->meta_tail, r->meta_tail, __ATOMIC_RELEASE);
+      if (!(d.flags & TF_DESC_HOST_RESERVED))
+        r->regions.push_back(HostRegion{d.payload_offset, tf_round_up16(d.payload_len),
+                                        d.skip_before, d.flags});
+    } else {
+      ++tail;
+    }
+    if (out) out[got] = d;
+    ++got;
+  }
+  *n = got;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_ready_entries(tf_ring* r, uint64_t* n) {
+  if (!r || !n) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  uint32_t k = 0;
+  int rc = tf_internal_poll(r, r->cfg.meta_slots, nullptr, &k, false);
+  *n = k;
+  return rc;
+}
+
+extern "C" int tf_ring_ready_bytes(tf_ring* r, uint64_t* n) {
+  if (!r || !n) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  uint64_t total = 0;
+  const uint64_t slots = r->cfg.meta_slots;
+  for (uint64_t i = 0; i < slots; ++i) {
+    uint64_t slot = (r->meta_tail + i) % slots;
+    if (slot_ready(r, slot) == TF_READY_SENTINEL) break;
+    total += reinterpret_cast<const uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE)[1];
+  }
+  *n = total;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_peek_ready(tf_ring* r, uint32_t max_entries, tf_descriptor* out, uint32_t* n) {
+  if (!r || !n) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  return tf_internal_poll(r, max_entries, out, n, false);
+}
+
+extern "C" int tf_ring_poll_ready(tf_ring* r, uint32_t max_entries, tf_descriptor* out, uint32_t* n) {
+  if (!r || !n) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  return tf_internal_poll(r, max_entries, out, n, true);
+}
+
+extern "C" int tf_ring_release_payload(tf_ring* r, uint64_t offset, uint64_t length) {
+  if (!r) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  if (r->regions.empty()) {  // rings.py:420-421
+    tf_set_error("no outstanding reservation to release");
+    return TF_ERR_OUT_OF_ORDER_RELEASE;
+  }
+  const HostRegion& h = r->regions.front();
+  if (h.off != offset || h.len != length) {  // rings.py:423-427
+    tf_set_error("release (%llu, %llu) does not match the oldest reservation (%llu, %llu)",
+                 (unsigned long long)offset, (unsigned long long)length,
+                 (unsigned long long)h.off, (unsigned long long)h.len);
+    return TF_ERR_OUT_OF_ORDER_RELEASE;
+  }
+  if (h.kind & TF_DESC_DEAD_SKIP) r->dead_reclaimed += h.skip;
+  r->L += h.skip + h.len;
+  r->bytes_released += h.len;
+  r->host_reserved.erase(h.off);
+  r->regions.pop_front();
+  __atomic_store_n(&r->cons->L, r->L, __ATOMIC_RELEASE);
+  return TF_OK;
+}
+
+static void producer_snapshot(const tf_ring* r, tf_pstate* p, uint64_t* meta_head) {
+  const volatile ProducerMirror* m = r->mirror;
+  p->V = m->V;
+  p->reset_mark = m->reset_mark;
+  p->reset_credit = m->reset_credit;
+  *meta_head = m->meta_head;
+}
+
+extern "C" int tf_ring_get_state(tf_ring* r, tf_ring_state* o) {
+  if (!r || !o) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  tf_pstate p;
+  uint64_t mh;
+  producer_snapshot(r, &p, &mh);
+  const uint64_t cap = r->cfg.payload_capacity;
+  const volatile ProducerMirror* m = r->mirror;
+  memset(o, 0, sizeof(*o));
+  o->payload_head = tf_head(&p, cap);
+  o->payload_tail = tf_tail(&p, r->L, cap);
+  o->occupancy = tf_used(&p, r->L);
+  o->payload_capacity = cap;
+  o->meta_head = mh;
+  o->meta_tail = r->meta_tail;
+  o->meta_slots = r->cfg.meta_slots;
+  o->high_watermark = r->cfg.high_watermark;
+  o->bytes_reserved = m->bytes_reserved;
+  o->bytes_released = r->bytes_released;
+  o->dead_created = m->dead_created;
+  o->dead_reclaimed = r->dead_reclaimed;
+  o->descriptors_published = mh;
+  o->descriptors_consumed = r->consumed;
+  o->captures_launched = m->captures;
+  o->drops = m->drops;
+  o->drop_bytes = m->drop_bytes;
+  o->stall_events = m->stall_events;
+  o->stall_ns = m->stall_ns;
+  o->device_errors = m->errors;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_free_meta_slots(tf_ring* r, uint64_t* n) {
+  if (!r || !n) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  *n = r->cfg.meta_slots - (r->mirror->meta_head - r->meta_tail);
+  return TF_OK;
+}
+
+// rings.py:256-276 would_fit: replay with a frozen consumer cursor.
+extern "C" int tf_ring_would_fit(tf_ring* r, const uint64_t* lengths, uint32_t n,
+                                 int64_t meta_entries, int* fits) {
+  if (!r || !fits || (n && !lengths)) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  tf_pstate p;
+  uint64_t mh;
+  producer_snapshot(r, &p, &mh);
+  const uint64_t cap = r->cfg.payload_capacity;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (lengths[i] == 0 || lengths[i] % TF_COPY_UNIT) {
+      tf_set_error("lengths must be positive copy-unit multiples");
+      return TF_ERR_VALUE;
+    }
+  }
+  *fits = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    uint64_t off, skip;
+    uint32_t kind;
+    if (!tf_reserve(&p, r->L, cap, lengths[i], &off, &skip, &kind)) return TF_OK;
+  }
+  uint64_t entries = meta_entries < 0 ? n : (uint64_t)meta_entries;
+  uint64_t free_slots = r->cfg.meta_slots - (mh - r->meta_tail);
+  *fits = entries <= free_slots;
+  return TF_OK;
+}
