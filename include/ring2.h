@@ -12,7 +12,8 @@
  *     1:1 onto the reference's exception classes (errors.py), and takes only
  *     plain pointers and integer sizes;
  *   - producer entry points (tf_capture) are launch-only: they enqueue work
- *     on the caller's CUDA stream, never synchronise it, and are legal
+ *     on the caller's CUDA stream (NULL = the legacy default stream, as in
+ *     the CUDA runtime), never synchronise it, and are legal
  *     inside CUDA-graph capture. Ring-full is reported through device
  *     counters and the result slot, not through the return code;
  *   - consumer entry points (poll/release/stager) run on host threads.

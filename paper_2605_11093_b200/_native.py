@@ -211,8 +211,7 @@ def lib() -> C.CDLL:
         if _lib is not None:
             return _lib
         from . import build_ext
-        if not _LIB_PATH.exists():
-            build_ext.build()
+        build_ext.build()  # no-op unless sources are newer than the .so
         if not _LIB_PATH.exists():  # pragma: no cover - build raises first
             raise RuntimeError(f"native library missing: {_LIB_PATH}")
         handle = C.CDLL(str(_LIB_PATH))

@@ -986,7 +986,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
   int grid = std::max(1, std::max(grid_bytes, grid_table));
   if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));
-  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (CUDA convention)
 
   if (a->op == TF_OP_COPY) {
     int vw = std::min<int>(sal, pow2_align((uint64_t)a->row_bytes));
@@ -1046,7 +1046,7 @@ extern "C" int tf_ring_reserve(tf_ring* r, void* stream, uint64_t length,
   if (length > r->cfg.payload_capacity) { tf_set_error("reservation exceeds payload capacity"); return TF_ERR_VALUE; }
   int rc = set_device(r->device);
   if (rc) return rc;
-  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (CUDA convention)
   CapParams P = base_params(r);
   reserve_kernel<<<1, 1, 0, s>>>(P, length);
   CUDA_TRY(cudaGetLastError());
@@ -1074,7 +1074,7 @@ extern "C" int tf_ring_publish(tf_ring* r, void* stream, const tf_descriptor* d,
   if (!r || !d) return TF_ERR_VALUE;
   int rc = set_device(r->device);
   if (rc) return rc;
-  cudaStream_t s = stream ? (cudaStream_t)stream : (cudaStream_t)r->own_stream;
+  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (CUDA convention)
   tf_descriptor dd = *d;
   if (dd.capture_seq == 0) {
     // user-built descriptor for a tf_ring_reserve'd region: its region is
