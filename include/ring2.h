@@ -243,7 +243,7 @@ typedef struct tf_drain_config {           /* exporter.py:35-51 */
   int32_t numa_node;                       /* -1 = auto from the GPU's PCI node */
   uint32_t stage_queue_slots;              /* exporter.py:32 (0 = 16) */
   uint32_t stage_threads;                  /* pinned->pageable copy threads (0 = auto) */
-  uint32_t _pad;
+  uint32_t discard_paged;                  /* 1: return pinned buffers without paging out (D2H-only measurement) */
 } tf_drain_config;
 
 typedef struct tf_stager tf_stager;
@@ -322,6 +322,8 @@ int tf_stager_free_paged(tf_stager* st, tf_paged_batch* batch);
 int tf_stager_note_sunk(tf_stager* st, uint64_t bytes);
 int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out);
 int tf_stager_error(tf_stager* st);       /* first background error, 0 if none */
+/* The staging stream (cudaStream_t) the D2H work is issued on. */
+int tf_stager_stream(tf_stager* st, void** stream);
 void tf_free_host(void* p);
 
 /* ---- measurement helpers (bench) ------------------------------------- */

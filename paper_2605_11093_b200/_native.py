@@ -116,7 +116,7 @@ class CDrainConfig(C.Structure):
                 ("staging_buffer_count", C.c_uint64), ("mode", C.c_uint32),
                 ("mapped_ctas", C.c_uint32), ("numa_node", C.c_int32),
                 ("stage_queue_slots", C.c_uint32),
-                ("stage_threads", C.c_uint32), ("_pad", C.c_uint32)]
+                ("stage_threads", C.c_uint32), ("discard_paged", C.c_uint32)]
 
 
 class CBatchInfo(C.Structure):
@@ -190,6 +190,7 @@ _SIGS = [
     ("tf_stager_note_sunk", C.c_int, [C.c_void_p, C.c_uint64]),
     ("tf_stager_stats_get", C.c_int, [C.c_void_p, C.POINTER(CStagerStats)]),
     ("tf_stager_error", C.c_int, [C.c_void_p]),
+    ("tf_stager_stream", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tf_free_host", None, [C.c_void_p]),
     ("tf_measure_d2h", C.c_int, [C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_double)]),
     ("tf_monotonic", C.c_double, []),

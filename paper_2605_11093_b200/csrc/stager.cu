@@ -677,6 +677,12 @@ extern "C" int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out) {
 
 extern "C" int tf_stager_error(tf_stager* st) { return st ? st->bg_error.load() : TF_ERR_VALUE; }
 
+extern "C" int tf_stager_stream(tf_stager* st, void** stream) {
+  if (!st || !stream) return TF_ERR_VALUE;
+  *stream = (void*)st->stream;
+  return TF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // background engine (wallclock.py:136-181 shape, real threads, no GIL)
 // ---------------------------------------------------------------------------
@@ -799,6 +805,14 @@ static void stage_loop(tf_stager* st) {
       if (st->to_stage.empty()) return;
       b = st->to_stage.front();
       st->to_stage.pop_front();
+      if (st->cfg.discard_paged) {
+        // D2H-only measurement: the bytes have landed in the pinned host
+        // ring; hand the buffer straight back.
+        st->stats.batches_staged += 1;
+        retire_batch(st, b);
+        st->cv.notify_all();
+        continue;
+      }
       dst = paged_alloc(st);
     }
     if (!dst) {

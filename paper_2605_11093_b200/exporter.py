@@ -50,6 +50,7 @@ class DrainConfig:
     numa_node: int = -1
     stage_threads: int = 0
     stage_queue_slots: int = STAGE_QUEUE_SLOTS
+    discard_paged: bool = False   # D2H-only measurement (no page-out / sink)
 
     def __post_init__(self) -> None:
         if min(self.min_ready_entries, self.min_ready_bytes) <= 0:
@@ -66,7 +67,8 @@ class DrainConfig:
             self.min_ready_entries, self.min_ready_bytes, self.max_wait,
             self.staging_buffer_size, self.staging_buffer_count,
             STAGING_MODES[self.mode], self.mapped_ctas, self.numa_node,
-            self.stage_queue_slots, self.stage_threads, 0)
+            self.stage_queue_slots, self.stage_threads,
+            1 if self.discard_paged else 0)
 
 
 class StagingBuffer:
@@ -160,7 +162,11 @@ class ExportPipeline:
     def __init__(self, ring: RingPair, config: DrainConfig | None = None,
                  engine: DeviceCopyEngine | None = None,
                  fifo: TensorMetaFIFO | None = None,
-                 hook_name_of=None) -> None:
+                 hook_name_of=None, copy_payloads: bool = True) -> None:
+        # copy_payloads=False hands sinks read-only views of the pageable
+        # batch (valid only during sink.write): for sinks that consume the
+        # bytes immediately (FileSink, NullSink, StreamSink).
+        self.copy_payloads = copy_payloads
         self.ring = ring
         self.config = config or DrainConfig()
         self.engine = engine or DeviceCopyEngine()
@@ -282,7 +288,7 @@ class ExportPipeline:
 
     def reconstruct(self, desc: Descriptor, payload) -> list[CaptureRecord]:
         meta = self.fifo.match(desc, self._hook_name_of(desc.hook_id))
-        return split_payload(meta, payload)
+        return split_payload(meta, payload, copy=self.copy_payloads)
 
     def sink_batch(self, batch: PageableBatch, sink, now: float = 0.0) -> None:
         total = 0
@@ -376,8 +382,14 @@ class ExportPipeline:
             self.pageable_bytes_in_flight += pb.bytes_total
             self.sink_batch(batch, self._sink, time.monotonic())
             self._sunk_batches_bg += 1
-        view.release()
+        del batch, view
         lib.tf_stager_free_paged(self._st, C.byref(pb))
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of the staging D2H work (for cross-stream events)."""
+        p = C.c_void_p()
+        N.check(N.lib().tf_stager_stream(self._st, C.byref(p)))
+        return int(p.value or 0)
 
     def _check_bg(self) -> None:
         if self._bg_error is not None:
@@ -390,6 +402,8 @@ class ExportPipeline:
         """Block until every published capture has been drained and sunk."""
         self._check_bg()
         N.check(N.lib().tf_stager_flush(self._st, timeout))
+        if self.config.discard_paged:
+            return
         deadline = time.monotonic() + timeout
         while True:
             self._check_bg()
@@ -416,8 +430,10 @@ class ExportPipeline:
             N.check(rc)
 
 
-def split_payload(meta: TensorMeta, payload) -> list[CaptureRecord]:
+def split_payload(meta: TensorMeta, payload, copy: bool = True) -> list[CaptureRecord]:
     """Per-request records of one capture payload, batch order kept."""
+    if not copy:
+        payload = memoryview(payload).toreadonly()
     if len(payload) != meta.expected_payload_len:
         raise MetaMismatch(
             f"payload {len(payload)} bytes != expected "
@@ -434,6 +450,7 @@ def split_payload(meta: TensorMeta, payload) -> list[CaptureRecord]:
             layer_index=meta.layer_index, step_seq=meta.step_seq,
             token_range=trange, shape=shape, dtype=meta.dtype,
             rank_coords=meta.rank_coords,
-            payload=bytes(payload[pos:pos + size])))
+            payload=bytes(payload[pos:pos + size]) if copy
+            else payload[pos:pos + size]))
         pos += size
     return out

@@ -1,0 +1,269 @@
+"""HookPoint and the per-device observation session (``Observer``).
+
+``HookPoint`` is the paper's instrumentation primitive (§3.1): an
+``nn.Module`` placed at an observation site whose forward is the identity
+plus a capture launch — no host synchronisation, no Python callback on the
+device timeline, legal inside CUDA-graph capture because the keep vector
+and the step sequence live in fixed device buffers that are rewritten
+between steps (§3.4 "index vector ... compatible with CUDA Graph
+replay").
+
+``Observer`` owns one ring pair, its export pipeline, the metadata FIFO and
+those device buffers, and implements the reference's per-step protocol
+(simulator.py:400-421 / wallclock.py:94-134):
+
+    plan = obs.begin_step(batch, step_seq)   # prepare_step, flush gate,
+                                             # FIFO entries, keep upload
+    model(...)                               # HookPoints launch captures
+    obs.end_step()                           # fence for the next snapshot
+
+Capture behaviour on a full ring follows the policy: completeness waits on
+the device for the consumer (the reference's in-step stall), best-effort
+drops and flags ``PolicyUnderestimate`` (which the plan makes impossible).
+
+Token-row sampling (north-star extension) keeps a per-token subset: a hook
+with ``sample=True`` captures rows (request, token) selected by the
+observer's ``TokenSampler``; its records carry ``row_counts`` and
+``token_indices``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from . import _native as N
+from ._device import torch
+from .errors import ConfigError, PolicyUnderestimate
+from .exporter import DrainConfig, ExportPipeline
+from .hooks import HookRegistry, RowSource, capture_args, launch_capture
+from .policy import PolicyConfig, StepPlan, prepare_step
+from .records import TensorMeta, TensorMetaFIFO
+from .rings import RingConfig, RingPair
+
+nn = torch().nn
+
+
+@dataclass(frozen=True)
+class TokenSampler:
+    """Which tokens of a request to keep: every ``every``-th, or a seeded
+    Bernoulli(``rate``) draw per (request, step)."""
+
+    every: int | None = None
+    rate: float | None = None
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        if (self.every is None) == (self.rate is None):
+            raise ConfigError("token sampler needs exactly one of every/rate")
+
+    def select(self, request_id: int, step_seq: int, tokens: int) -> list[int]:
+        if self.every is not None:
+            return list(range(0, tokens, self.every))
+        import random
+        rng = random.Random((self.seed << 40) ^ (request_id << 20) ^ step_seq)
+        return [t for t in range(tokens) if rng.random() < self.rate]
+
+
+class Observer:
+    """One device's capture session: ring, exporter, policy, keep buffers."""
+
+    def __init__(self, registry: HookRegistry, *, ring: RingConfig,
+                 drain: DrainConfig | None = None,
+                 policy: PolicyConfig | None = None, sink=None,
+                 device: int | None = None, max_batch: int = 1024,
+                 max_tokens: int = 8192, max_rows_sampled: int = 1 << 22,
+                 sampler: TokenSampler | None = None,
+                 sampled_hooks: frozenset = frozenset(),
+                 rank_coords: tuple = (0, 0), wait_timeout: float = 60.0):
+        t = torch()
+        self.registry = registry
+        self.policy = policy or PolicyConfig()
+        self.ring = RingPair(ring, device=device, wait_timeout=wait_timeout)
+        self.device = self.ring.device
+        self.fifo = TensorMetaFIFO()
+        self.exporter = ExportPipeline(
+            self.ring, drain or DrainConfig(), None, self.fifo,
+            hook_name_of=lambda h: registry.hook(h).name)
+        self.sink = sink
+        self.sampler = sampler
+        self.sampled_hooks = frozenset(sampled_hooks)
+        self.rank_coords = rank_coords
+        dev = f"cuda:{self.device}"
+        self.keep_req = t.ones(max_batch, dtype=t.uint8, device=dev)
+        self.keep_tok = t.zeros(max(1, max_rows_sampled), dtype=t.uint8,
+                                device=dev)
+        self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
+        self.max_batch = max_batch
+        self._names = {h.name: i for i, h in enumerate(registry.hooks)}
+        self._plan: StepPlan | None = None
+        self._batch = []
+        self._tok_sel: dict[int, list[int]] = {}
+        self.active = False
+        self.launches = 0
+        self.steps = 0
+
+    # -- session -----------------------------------------------------------
+
+    def start(self) -> "Observer":
+        if self.sink is not None and not self.exporter.running:
+            self.exporter.start(self.sink)
+        return self
+
+    def stop(self, flush: bool = True) -> None:
+        if self.exporter.running:
+            self.exporter.stop(flush=flush)
+
+    def close(self) -> None:
+        self.stop()
+        self.exporter.close()
+        self.ring.close()
+
+    def flush(self, timeout: float = 120.0) -> None:
+        self.ring.sync()
+        self.exporter.flush(timeout)
+
+    # -- per step --------------------------------------------------------------
+
+    def begin_step(self, batch, step_seq: int, stream=None) -> StepPlan:
+        """Plan the step, honour the flush gate, queue metadata, upload keep."""
+        t = torch()
+        batch = list(batch)
+        if len(batch) > self.max_batch:
+            raise ConfigError("batch exceeds the observer's max_batch")
+        self.registry.commit_filter()
+        plan = prepare_step(self.policy, batch, self.ring, self.registry,
+                            step_seq=step_seq, rank_coords=self.rank_coords)
+        if plan.flush_before:
+            self.flush()
+        metas = list(plan.fifo_entries)
+        sel = {}
+        if self.sampler is not None and plan.kept_ids and self.sampled_hooks:
+            kept = [r for r in batch if r.request_id in set(plan.kept_ids)]
+            for r in kept:
+                sel[r.request_id] = self.sampler.select(r.request_id, step_seq,
+                                                        r.tokens)
+            metas = [self._sampled_meta(m, kept, sel)
+                     if m.hook_name in self._sampled_names() else m
+                     for m in metas]
+        self.fifo.extend(metas)
+        s = stream if stream is not None else t.cuda.current_stream(self.device)
+        with t.cuda.stream(s):
+            keep = t.tensor(list(plan.keep) or [0], dtype=t.uint8).pin_memory()
+            self.keep_req[:keep.numel()].copy_(keep, non_blocking=True)
+            step = t.tensor([step_seq & 0x7FFFFFFF], dtype=t.int32).pin_memory()
+            self.step_buf.copy_(step, non_blocking=True)
+            if sel:
+                tokens = batch[0].tokens
+                flags = [0] * (len(batch) * tokens)
+                for i, r in enumerate(batch):
+                    for tok in sel.get(r.request_id, ()):
+                        flags[i * tokens + tok] = 1
+                kt = t.tensor(flags, dtype=t.uint8).pin_memory()
+                self.keep_tok[:kt.numel()].copy_(kt, non_blocking=True)
+        self._plan, self._batch, self._tok_sel = plan, batch, sel
+        self.active = bool(plan.kept_ids)
+        self.steps += 1
+        return plan
+
+    def end_step(self, stream=None) -> None:
+        self.ring.note_launch(stream)
+        self.active = False
+
+    def check_device(self) -> None:
+        """Raise if the device dropped a capture the plan admitted."""
+        st = self.ring.state()
+        if st.device_errors & N.TF_DEVERR_UNDERESTIMATE:
+            raise PolicyUnderestimate(
+                f"{st.drops} capture(s) dropped on a full ring")
+        if st.device_errors & N.TF_DEVERR_TIMEOUT:
+            from .errors import DeviceError
+            raise DeviceError("device wait for ring space timed out")
+
+    def _sampled_names(self) -> set:
+        return {self.registry.hook(h).name for h in self.sampled_hooks}
+
+    def _sampled_meta(self, meta: TensorMeta, kept, sel) -> TensorMeta:
+        counts = tuple(len(sel[r.request_id]) for r in kept)
+        per_row_shape = tuple(meta.shape[1:])
+        return TensorMeta(
+            hook_name=meta.hook_name, layer_index=meta.layer_index,
+            step_seq=meta.step_seq, request_ids=meta.request_ids,
+            token_ranges=meta.token_ranges,
+            shape=(max(1, max(counts, default=1)),) + per_row_shape,
+            dtype=meta.dtype, rank_coords=meta.rank_coords,
+            row_counts=counts,
+            token_indices=tuple(tuple(sel[r.request_id]) for r in kept))
+
+    # -- capture (called by HookPoint) -------------------------------------
+
+    def hook_id(self, name: str) -> int | None:
+        return self._names.get(name)
+
+    def capture(self, hook_id: int, x, stream=None) -> None:
+        """Launch the capture of ``x`` (batch-major (B, T, ...)) for this step."""
+        if not self.active or not self.registry.is_enabled(hook_id):
+            return
+        hook = self.registry.hook(hook_id)
+        src = _rows_of(x, hook)
+        sampled = hook_id in self.sampled_hooks and self._tok_sel
+        args = capture_args(
+            src, hook_id=hook_id, hook=hook,
+            keep_ptr=(self.keep_tok if sampled else self.keep_req).data_ptr(),
+            keep_per_outer=not sampled, step_seq_ptr=self.step_buf.data_ptr(),
+            full=self.policy.full_mode)
+        launch_capture(self.ring, args, stream)
+        self.launches += 1
+
+
+def _rows_of(x, hook) -> RowSource:
+    """Describe a (B, T, ..., H) activation as strided rows (b, t)."""
+    if x.dim() < 2:
+        raise ConfigError("captured activations are batch-major (B, ...)")
+    esz = x.element_size()
+    if x.dim() == 2:
+        x2 = x if x.stride(-1) == 1 else x.contiguous()
+        return RowSource(x2.data_ptr(), x2.shape[0], 1, x2.shape[1] * esz,
+                         x2.stride(0) * esz, x2.shape[1] * esz, x2)
+    b = x.shape[0]
+    inner = x[0]
+    if not inner.is_contiguous() or x.stride(-1) != 1:
+        x = x.contiguous()
+        inner = x[0]
+    row_elems = x.shape[-1]
+    mid = inner.numel() // row_elems
+    return RowSource(x.data_ptr(), b, mid, row_elems * esz, x.stride(0) * esz,
+                     row_elems * esz, x)
+
+
+class HookPoint(nn.Module):
+    """Identity module that captures its input into the observer's ring."""
+
+    def __init__(self, name: str, observer: Observer | None = None) -> None:
+        super().__init__()
+        self.name = name
+        self.observer = observer
+        self._hid = observer.hook_id(name) if observer is not None else None
+
+    def bind(self, observer: Observer) -> None:
+        self.observer = observer
+        self._hid = observer.hook_id(self.name)
+
+    def forward(self, x):
+        obs = self.observer
+        if obs is not None and self._hid is not None and obs.active:
+            obs.capture(self._hid, x)
+        return x
+
+
+def total_step_bytes(registry: HookRegistry, batch) -> int:
+    from .policy import estimate_step_bytes
+    return sum(estimate_step_bytes(registry, batch))
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+__all__ = ["HookPoint", "Observer", "TokenSampler", "total_step_bytes",
+           "ceil_div", "math"]

@@ -1,0 +1,147 @@
+"""HookPoint placement for Hugging Face models (§4 "Framework
+integration": observation sites declared once, HookPoints attached without
+editing the backbone).
+
+Sites (per decoder layer ``L``):
+
+    resid_post[L]   decoder-layer output (B, T, H)            residual stream
+    mlp_act[L]      input of down_proj: act(gate) * up (B, T, F)   MLP
+    attn_out[L]     self-attention output before the residual add (B, T, H)
+    attn_pattern[L] attention probabilities (B, heads, T, T)  (eager attention)
+    k_slice[L]      k_proj output for this step's tokens (B, T, kv*d), pre-RoPE
+    v_slice[L]      v_proj output (B, T, kv*d)  — the V rows the cache stores
+
+Each site becomes a ``HookPoint`` submodule registered on the model (so it
+shows in ``named_modules``) and driven from a forward hook on the module
+that produces the tensor. Declaration order inside a layer follows
+execution order: attn sites, then mlp_act, then resid_post.
+"""
+
+from __future__ import annotations
+
+from .hookpoint import HookPoint, Observer
+from .hooks import DType, HookSpec, ModelSpec, install_hooks
+
+SITE_ORDER = ("k_slice", "v_slice", "attn_pattern", "attn_out", "mlp_act",
+              "resid_post")
+
+_TORCH_TO_DTYPE = {"torch.bfloat16": "bf16", "torch.float16": "f16",
+                   "torch.float32": "f32"}
+
+
+def llama_specs(config, sites, dtype: str = "bf16", cast_to=None,
+                reduce=None) -> list[HookSpec]:
+    """Per-layer HookSpecs for a Llama-family config, in firing order."""
+    dt = DType.of(dtype)
+    kv = config.num_key_value_heads * (config.hidden_size //
+                                       config.num_attention_heads)
+    dims = {
+        "resid_post": ("tokens", "hidden"),
+        "attn_out": ("tokens", "hidden"),
+        "mlp_act": ("tokens", config.intermediate_size),
+        "k_slice": ("tokens", kv),
+        "v_slice": ("tokens", kv),
+        "attn_pattern": (config.num_attention_heads, "tokens", "tokens"),
+    }
+    out = []
+    for site in SITE_ORDER:
+        if site in sites:
+            out.append(HookSpec(site, dims[site], dt, per_layer=True,
+                                cast_to=DType.of(cast_to) if cast_to else None,
+                                reduce=reduce))
+    return out
+
+
+def gpt2_specs(config, dtype: str = "f32") -> list[HookSpec]:
+    return [HookSpec("resid_post", ("tokens", "hidden"), DType.of(dtype),
+                     per_layer=True)]
+
+
+def llama_registry(config, sites, dtype: str = "bf16", **kw):
+    model = ModelSpec(config.num_hidden_layers, config.hidden_size)
+    return install_hooks(model, llama_specs(config, sites, dtype, **kw))
+
+
+def _first(out):
+    return out[0] if isinstance(out, (tuple, list)) else out
+
+
+def attach_llama(model, observer: Observer | None, sites) -> list:
+    """Insert HookPoints into a HF Llama model; returns the hook handles."""
+    inner = getattr(model, "model", model)
+    handles = []
+    for L, layer in enumerate(inner.layers):
+        def add(site):
+            hp = HookPoint(f"{site}[{L}]", observer)
+            model.add_module(f"hookpoint_{site}_{L}", hp)
+            return hp
+        if "resid_post" in sites:
+            hp = add("resid_post")
+            handles.append(layer.register_forward_hook(
+                lambda m, a, out, hp=hp: (hp(_first(out)), None)[1]))
+        if "mlp_act" in sites:
+            hp = add("mlp_act")
+            handles.append(layer.mlp.down_proj.register_forward_pre_hook(
+                lambda m, args, hp=hp: (hp(args[0]), None)[1]))
+        if "attn_out" in sites:
+            hp = add("attn_out")
+            handles.append(layer.self_attn.register_forward_hook(
+                lambda m, a, out, hp=hp: (hp(_first(out)), None)[1]))
+        if "attn_pattern" in sites:
+            hp = add("attn_pattern")
+            handles.append(layer.self_attn.register_forward_hook(
+                lambda m, a, out, hp=hp: (hp(out[1]) if out[1] is not None
+                                          else None, None)[1]))
+        if "k_slice" in sites:
+            hp = add("k_slice")
+            handles.append(layer.self_attn.k_proj.register_forward_hook(
+                lambda m, a, out, hp=hp: (hp(out), None)[1]))
+        if "v_slice" in sites:
+            hp = add("v_slice")
+            handles.append(layer.self_attn.v_proj.register_forward_hook(
+                lambda m, a, out, hp=hp: (hp(out), None)[1]))
+    return handles
+
+
+def attach_gpt2(model, observer: Observer | None) -> list:
+    """resid_post[L] on every GPT-2 block output."""
+    inner = getattr(model, "transformer", model)
+    handles = []
+    for L, block in enumerate(inner.h):
+        hp = HookPoint(f"resid_post[{L}]", observer)
+        model.add_module(f"hookpoint_resid_post_{L}", hp)
+        handles.append(block.register_forward_hook(
+            lambda m, a, out, hp=hp: (hp(_first(out)), None)[1]))
+    return handles
+
+
+def detach(handles) -> None:
+    for h in handles:
+        h.remove()
+
+
+def random_llama(config, device: str = "cuda", dtype=None, seed: int = 0):
+    """Random-init Llama built directly on the device in bf16 (no weights)."""
+    import torch
+    from transformers import LlamaForCausalLM
+    dtype = dtype or torch.bfloat16
+    torch.manual_seed(seed)
+    prev = torch.get_default_dtype()
+    torch.set_default_dtype(dtype)
+    try:
+        with torch.device(device):
+            model = LlamaForCausalLM(config)
+    finally:
+        torch.set_default_dtype(prev)
+    return model.eval()
+
+
+def llama3_8b_config(layers: int | None = None, attn: str = "sdpa"):
+    from transformers import LlamaConfig
+    cfg = LlamaConfig(hidden_size=4096, intermediate_size=14336,
+                      num_hidden_layers=32 if layers is None else layers,
+                      num_attention_heads=32, num_key_value_heads=8,
+                      vocab_size=128256, max_position_embeddings=8192,
+                      rope_theta=500000.0, rms_norm_eps=1e-5)
+    cfg._attn_implementation = attn
+    return cfg
