@@ -204,7 +204,6 @@ def leg_value(args, dist, dev):
                         staging_buffer_count=6, mode=args.staging,
                         discard_paged=True)
     pipe = ExportPipeline(ring, drain)
-    pipe.start(sink=None)
     keep = torch.ones(B, dtype=torch.uint8, device=dev)
     prod = torch.cuda.Stream(device=dev)
     cap_args = []
@@ -227,8 +226,25 @@ def leg_value(args, dist, dev):
             if events is not None:
                 events[i][1].record(prod)
 
+    # roofline pass: one step of captures into an empty ring with the
+    # staging engine idle, each launch bracketed by CUDA events on the
+    # producer stream (the timed region below waits on PCIe by design)
+    run_step(0)                       # cold launch / module load
+    prod.synchronize()
+    pipe.start(sink=None)
+    pipe.flush(120)
+    pipe.stop(flush=True)
+    roof_ev = [(torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(n_caps)]
+    k0 = ring.state().kernel_ns
+    run_step(1, roof_ev)
+    prod.synchronize()
+    ring.note_launch(prod)
+    roof_dev_ns = (ring.state().kernel_ns - k0) / n_caps
+    roof_ms = [a.elapsed_time(b) for a, b in roof_ev]
+    pipe.start(sink=None)
     for w in range(args.warmup):
-        run_step(w)
+        run_step(2 + w)
     prod.synchronize()
     pipe.flush(120)
     stager_stream = torch.cuda.ExternalStream(pipe.stream_handle(), device=dev)
@@ -254,14 +270,17 @@ def leg_value(args, dist, dev):
     stats1 = pipe.stats()
     elapsed = start.elapsed_time(end) * 1e-3
     staged = stats1["bytes_drained"] - stats0["bytes_drained"]
-    kernel_ms = [a.elapsed_time(b) for step in ev_pairs for a, b in step]
-    per_launch = [nb for _ in range(args.steps) for _, nb in cap_args]
+    kernel_ms = roof_ms
+    per_launch = [nb for _, nb in cap_args]
+    timed_kernel_ms = [a.elapsed_time(b) for step in ev_pairs for a, b in step]
     state = ring.state()
     pipe.stop(flush=True)
     out = {
         "staged_bytes": staged, "elapsed_s": elapsed,
         "step_bytes": step_bytes, "captures_per_step": n_caps,
         "kernel_ms": kernel_ms, "launch_bytes": per_launch,
+        "kernel_dev_us": roof_dev_ns / 1e3,
+        "timed_kernel_avg_us": sum(timed_kernel_ms) / len(timed_kernel_ms) * 1e3,
         "d2h_seconds": stats1["transfer_seconds"] - stats0["transfer_seconds"],
         "stall_events": state.stall_events, "drops": state.drops,
         "clocks": clocks.summary(),
@@ -370,57 +389,85 @@ def leg_model(args, dist, dev):
     def fwd():
         model.model(input_ids=ids, use_cache=False)
 
-    def timed(n, obs=None, base=0):
-        times = []
+    def make_graph():
+        """Prefill step as one CUDA graph (HookPoints, if attached and the
+        observer is active, are recorded into it)."""
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            for _ in range(2):
+                fwd()
+        stream.wait_stream(cs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.inference_mode(), torch.cuda.graph(graph):
+            model.model(input_ids=ids, use_cache=False)
+        return graph
+
+    def run(n, step_fn, obs=None, base=0):
+        """n back-to-back steps (the host plans step k+1 while the device
+        runs step k); device time over the whole region per step."""
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         for s in range(n):
             if obs is not None:
                 obs.begin_step(batch, base + s)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fwd()
-            b.record(stream)
+            step_fn()
             if obs is not None:
                 obs.end_step(stream)
-            b.synchronize()
-            times.append(a.elapsed_time(b))
-        return times
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / n
 
-    for _ in range(args.warmup):
-        fwd()
-    torch.cuda.synchronize(dev)
     n = max(3, args.steps)
-    base = timed(n)
-    results = {"no_capture_ms": statistics.median(base)}
-    for label, sites in (("resid", ("resid_post",)),
-                         ("resid_mlp", ("mlp_act", "resid_post"))):
-        reg = llama_registry(cfg, sites)
-        step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
-        sink = NullSink()
-        obs = Observer(reg, ring=RingConfig(min(24 * GiB, 4 * step_bytes), 1024),
-                       drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
-                                         max_wait=1e-4,
-                                         staging_buffer_size=128 << 20,
-                                         staging_buffer_count=6,
-                                         mode=args.staging, stage_threads=4),
-                       policy=PolicyConfig(), sink=sink, device=dev.index,
-                       max_batch=B)
-        obs.exporter.copy_payloads = False
-        obs.start()
-        handles = attach_llama(model, obs, sites)
-        timed(args.warmup, obs, 0)
-        obs.flush(300)
-        times = timed(n, obs, 1000)
-        t_run = sum(times)
-        obs.flush(600)
-        st = obs.ring.state()
-        obs.check_device()
-        detach(handles)
-        obs.close()
-        results[label] = {
-            "capture_ms": statistics.median(times),
-            "overhead_pct": (t_run - sum(base)) / sum(base) * 100.0,
-            "step_bytes": step_bytes, "stall_events": st.stall_events,
-            "records": sink.records_written}
+    results = {}
+    for mode in ("graph", "eager"):
+        for _ in range(args.warmup):
+            fwd()
+        g0 = make_graph() if mode == "graph" else None
+        step0 = g0.replay if g0 is not None else fwd
+        run(2, step0)
+        base = run(n, step0)
+        res = {"no_capture_ms": base}
+        for label, sites in (("resid", ("resid_post",)),
+                             ("resid_mlp", ("mlp_act", "resid_post"))):
+            reg = llama_registry(cfg, sites)
+            step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
+            sink = NullSink()
+            obs = Observer(reg, ring=RingConfig(min(24 * GiB, 4 * step_bytes), 1024),
+                           drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
+                                             max_wait=1e-4,
+                                             staging_buffer_size=128 << 20,
+                                             staging_buffer_count=6,
+                                             mode=args.staging, stage_threads=4),
+                           policy=PolicyConfig(), sink=sink, device=dev.index,
+                           max_batch=B)
+            obs.exporter.copy_payloads = False
+            obs.start()
+            handles = attach_llama(model, obs, sites)
+            if mode == "graph":
+                obs.begin_step(batch, 0)   # active while recording the graph
+                g1 = make_graph()
+                obs.end_step(stream)
+                step1 = g1.replay
+            else:
+                g1, step1 = None, fwd
+            obs.flush(300)
+            run(max(1, args.warmup - 1), step1, obs, 100)
+            obs.flush(300)
+            t = run(n, step1, obs, 1000)   # run time stops at inference end
+            obs.flush(600)                 # export tail, reported apart
+            st = obs.ring.state()
+            obs.check_device()
+            detach(handles)
+            obs.close()
+            del g1
+            res[label] = {
+                "capture_ms": t, "overhead_pct": (t - base) / base * 100.0,
+                "step_bytes": step_bytes, "stall_events": st.stall_events,
+                "records": sink.records_written}
+        del g0
+        results[mode] = res
     del model
     torch.cuda.empty_cache()
     return results
@@ -590,9 +637,10 @@ def main():
                "steps": e["steps"], "records": e["records"]}
     model = leg_model(args, dist, dev) if "model" in legs else None
     if model:
-        for key in ("resid", "resid_mlp"):
-            model[key]["overhead_pct_max_over_ranks"] = dist.reduce(
-                [model[key]["overhead_pct"]], "max")[0]
+        for mode in model:
+            for key in ("resid", "resid_mlp"):
+                model[mode][key]["overhead_pct_max_over_ranks"] = dist.reduce(
+                    [model[mode][key]["overhead_pct"]], "max")[0]
     cpu = cpu_baseline(args.batch, args.seq) if ("cpu" in legs and dist.world == 1
                                                   and dist.rank == 0) else None
 
@@ -621,7 +669,13 @@ def main():
                          "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "capture_kernel<COPY,16>",
                          "avg_launch_us": avg_ms * 1e3,
-                         "algorithmic_bytes_per_launch": avg_alg},
+                         "avg_launch_us_device_timer": v["kernel_dev_us"],
+                         "avg_launch_us_in_timed_region": v["timed_kernel_avg_us"],
+                         "algorithmic_bytes_per_launch": avg_alg,
+                         "note": "event-timed launches of one 64-capture step "
+                                 "(resid 32 MiB + mlp 112 MiB per layer) into an "
+                                 "empty ring, staging idle; inside the timed "
+                                 "region launches also wait for ring space"},
             "staging_roofline": {"bound": "pcie", "achieved": d2h_gbs,
                                  "peak": pcie_peak, "unit": "GB/s",
                                  "frac": d2h_gbs / pcie_peak if d2h_gbs else None,

@@ -69,7 +69,8 @@ typedef struct tf_descriptor {
   uint32_t flags;          /* @40 TF_DESC_* */
   uint32_t n_rows;         /* @44 rows gathered into the payload */
   uint64_t capture_seq;    /* @48 producer launch counter */
-  uint64_t reserved1;      /* @56 */
+  uint64_t checksum;       /* @56 mix of words 0..6; the host accepts a slot
+                              only when it verifies (no fence on publish) */
 } tf_descriptor;
 
 #define TF_DESC_DEAD_SKIP 0x1u     /* skip_before bytes are a dead region */
@@ -107,6 +108,8 @@ typedef struct tf_ring_state {
   uint64_t stall_events;      /* waits under TF_FULL_WAIT */
   uint64_t stall_ns;
   uint64_t device_errors;     /* bitmask of TF_DEVERR_* */
+  uint64_t kernel_ns;         /* sum of capture-kernel durations (device globaltimer) */
+  uint64_t last_kernel_ns;    /* duration of the most recent capture kernel */
 } tf_ring_state;
 
 #define TF_DEVERR_UNDERESTIMATE 0x1u /* drop under TF_FULL_DROP (best effort) */
@@ -219,6 +222,9 @@ int tf_ring_peek_ready(tf_ring* ring, uint32_t max_entries,
 int tf_ring_poll_ready(tf_ring* ring, uint32_t max_entries,
                        tf_descriptor* out, uint32_t* n);
 int tf_ring_release_payload(tf_ring* ring, uint64_t offset, uint64_t length);
+/* Wait until the device sees every release/poll made so far (the cursors
+ * reach device memory through stream-ordered writes). */
+int tf_ring_sync_consumer(tf_ring* ring);
 
 /* ---- shared: rings.py:241-276 ------------------------------------------ */
 /* Snapshot; the caller must have synchronised the producer stream. */

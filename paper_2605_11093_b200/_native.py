@@ -71,7 +71,7 @@ class CDescriptor(C.Structure):
                 ("hook_id", C.c_uint32), ("step_seq", C.c_uint32),
                 ("ready_seq", C.c_uint64), ("skip_before", C.c_uint64),
                 ("flags", C.c_uint32), ("n_rows", C.c_uint32),
-                ("capture_seq", C.c_uint64), ("reserved1", C.c_uint64)]
+                ("capture_seq", C.c_uint64), ("checksum", C.c_uint64)]
 
 
 class CRingConfig(C.Structure):
@@ -88,7 +88,7 @@ class CRingState(C.Structure):
             "bytes_reserved", "bytes_released", "dead_created",
             "dead_reclaimed", "descriptors_published", "descriptors_consumed",
             "captures_launched", "drops", "drop_bytes", "stall_events",
-            "stall_ns", "device_errors")]
+            "stall_ns", "device_errors", "kernel_ns", "last_kernel_ns")]
 
 
 class CCaptureArgs(C.Structure):
@@ -169,6 +169,7 @@ _SIGS = [
     ("tf_ring_peek_ready", C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(CDescriptor), u32p]),
     ("tf_ring_poll_ready", C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(CDescriptor), u32p]),
     ("tf_ring_release_payload", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    ("tf_ring_sync_consumer", C.c_int, [C.c_void_p]),
     ("tf_ring_get_state", C.c_int, [C.c_void_p, C.POINTER(CRingState)]),
     ("tf_ring_free_meta_slots", C.c_int, [C.c_void_p, u64p]),
     ("tf_ring_would_fit", C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_int64, C.POINTER(C.c_int)]),

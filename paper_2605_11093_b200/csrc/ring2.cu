@@ -5,9 +5,15 @@
 //   capture()         hooks.py:281-324   -> capture_kernel (one launch)
 //   _gather_compact   hooks.py:266-278   -> ordered compaction + 128-bit copy
 //   reserve_payload   rings.py:286-319   -> leader CTA, tf_reserve (ring2_core.h)
-//   publish           rings.py:321-353   -> last CTA: body, fence, ready_seq
+//   publish           rings.py:321-353   -> last CTA: one coalesced 64-B post
 //   poll_ready        rings.py:380-406   -> tf_ring_poll_ready (host)
 //   release_payload   rings.py:408-431   -> tf_ring_release_payload (host)
+//
+// Placement rule learned on the box: while the staging D2H saturates PCIe,
+// anything a kernel on the inference stream does with host memory (reads,
+// system fences, scattered stores) waits behind that traffic. The capture
+// kernel therefore reads only device memory and posts exactly one 64-byte
+// descriptor (checksummed, no fence) to the mapped meta ring.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -16,6 +22,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <time.h>
@@ -93,6 +100,11 @@ extern "C" int tf_plan_reservation(uint64_t head, uint64_t tail, uint64_t used,
 // ---------------------------------------------------------------------------
 namespace {
 
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -100,9 +112,6 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
 }
 __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
@@ -119,7 +128,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// streaming 128-bit loads: source activations are read exactly once
+// streaming loads: source activations are read exactly once
 template <int VW> struct VecT;
 template <> struct VecT<16> { using T = uint4; };
 template <> struct VecT<8> { using T = uint2; };
@@ -267,10 +276,8 @@ struct CapParams {
   uint8_t* payload;
   uint64_t cap;
   uint64_t slots;
-  uint8_t* meta;
-  const ConsumerShared* cons;
-  ProducerMirror* mirror;
-  tf_capture_result* result;
+  uint8_t* meta;              // mapped host memory (descriptors only)
+  const DevConsumer* dcons;
   DevCtl* ctl;
   uint64_t timeout_ns;
 };
@@ -283,6 +290,9 @@ struct CapShared {
   uint32_t status;
   uint64_t off;
   uint32_t is_last;
+  uint32_t publish;
+  uint64_t desc[8];
+  uint64_t* slot;
   uint32_t table[kTableMax];
 };
 
@@ -318,8 +328,8 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, CapShared& 
   return sh.warp_sums[warp] + x - v;
 }
 
-// Leader: reservation against a fresh consumer snapshot (rings.py:286-319,
-// hooks.py:313-315: meta availability first, then payload).
+// Leader: reservation against the device view of the consumer cursors
+// (rings.py:286-319; hooks.py:313-315: meta availability first, then payload).
 __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows) {
   DevCtl* c = P.ctl;
   const uint32_t mode = P.flags & TF_FULL_MASK;
@@ -342,8 +352,8 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
   uint64_t t0 = 0;
   bool stalled = false;
   for (;;) {
-    uint64_t L = ld_relaxed_sys(&P.cons->L);
-    uint64_t mtail = ld_relaxed_sys(&P.cons->meta_tail);
+    uint64_t L = ld_relaxed_gpu(&P.dcons->L);
+    uint64_t mtail = ld_relaxed_gpu(&P.dcons->meta_tail);
     bool meta_ok = (c->meta_head - mtail) < P.slots;
     uint32_t status = TF_ERR_META_RING_FULL;
     if (meta_ok) {
@@ -363,7 +373,7 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
       }
       status = TF_ERR_PAYLOAD_RING_FULL;
     }
-    if (mode == TF_FULL_WAIT) {
+    if (mode == TF_FULL_WAIT) {  // completeness: stall in-step (simulator.py:384-393)
       uint64_t now = globaltimer();
       if (!stalled) {
         stalled = true;
@@ -377,7 +387,7 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
         c->plan_status = TF_ERR_TIMEOUT;
         return;
       }
-      __nanosleep(2000);
+      __nanosleep(1000);
       continue;
     }
     if (mode == TF_FULL_DROP) {
@@ -390,30 +400,14 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
   }
 }
 
-__device__ void write_mirror(const CapParams& P) {
+// Last CTA, thread 0: build the descriptor and the result record; the
+// caller posts the descriptor with one coalesced warp store.
+__device__ void last_cta_prepare(const CapParams& P, CapShared& sh) {
   DevCtl* c = P.ctl;
-  ProducerMirror* m = P.mirror;
-  st_relaxed_sys(&m->V, c->p.V);
-  st_relaxed_sys(&m->reset_mark, c->p.reset_mark);
-  st_relaxed_sys(&m->reset_credit, c->p.reset_credit);
-  st_relaxed_sys(&m->meta_head, c->meta_head);
-  st_relaxed_sys(&m->bytes_reserved, c->bytes_reserved);
-  st_relaxed_sys(&m->dead_created, c->dead_created);
-  st_relaxed_sys(&m->captures, c->captures);
-  st_relaxed_sys(&m->drops, c->drops);
-  st_relaxed_sys(&m->drop_bytes, c->drop_bytes);
-  st_relaxed_sys(&m->stall_events, c->stall_events);
-  st_relaxed_sys(&m->stall_ns, c->stall_ns);
-  st_relaxed_sys(&m->errors, c->errors);
-  st_relaxed_sys(&m->capture_seq, c->capture_seq);
-}
-
-// Last CTA: descriptor body, system fence, ready_seq release store
-// (rings.py:321-353; "last retiring block").
-__device__ void last_cta_publish(const CapParams& P) {
-  DevCtl* c = P.ctl;
-  tf_capture_result* res = P.result;
   const uint32_t status = c->plan_status;
+  const uint64_t dt = globaltimer() - c->k_t0;
+  c->last_kernel_ns = dt;
+  c->kernel_ns += dt;
   tf_descriptor d;
   d.payload_offset = c->plan_off;
   d.payload_len = c->plan_bytes;
@@ -424,41 +418,27 @@ __device__ void last_cta_publish(const CapParams& P) {
   d.flags = c->plan_kind;
   d.n_rows = (uint32_t)c->plan_rows;
   d.capture_seq = c->plan_seq;
-  d.reserved1 = 0;
+  d.checksum = 0;
+  sh.publish = 0;
   if (status == TF_OK && !(P.flags & TF_CAP_DEFER_PUBLISH)) {
-    uint64_t seq = c->meta_head;
-    uint64_t slot = seq % P.slots;
-    uint64_t* w = reinterpret_cast<uint64_t*>(P.meta + slot * TF_DESCRIPTOR_SIZE);
-    const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
-    __threadfence_system();  // payload of every CTA before the descriptor
-    st_relaxed_sys(w + 0, s[0]);
-    st_relaxed_sys(w + 1, s[1]);
-    st_relaxed_sys(w + 2, s[2]);
-    st_relaxed_sys(w + 4, s[4]);
-    st_relaxed_sys(w + 5, s[5]);
-    st_relaxed_sys(w + 6, s[6]);
-    st_relaxed_sys(w + 7, s[7]);
-    st_release_sys(w + 3, seq);  // ready_seq last
+    const uint64_t seq = c->meta_head;
     d.ready_seq = seq;
+    d.checksum = tf_desc_checksum(reinterpret_cast<const uint64_t*>(&d));
+    sh.slot = reinterpret_cast<uint64_t*>(P.meta + (seq % P.slots) * TF_DESCRIPTOR_SIZE);
+    sh.publish = 1;
     c->meta_head = seq + 1;
   }
-  write_mirror(P);
-  // result slot
-  const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
-  uint64_t* rd = reinterpret_cast<uint64_t*>(&res->desc);
-  for (int i = 0; i < 8; ++i) st_relaxed_sys(rd + i, s[i]);
-  st_relaxed_sys(&res->payload_offset, status == TF_OK ? c->plan_off : 0);
-  st_relaxed_sys(&res->payload_len, status == TF_OK ? c->plan_bytes : 0);
-  st_relaxed_sys(&res->skip_before, c->plan_skip);
-  st_relaxed_sys(&res->ready_seq, d.ready_seq);
-  st_relaxed_sys(reinterpret_cast<uint64_t*>(&res->status),
-                 uint64_t(status) | (uint64_t(c->plan_rows) << 32));
-  st_release_sys(&res->capture_seq, c->plan_seq);
-  // re-arm the handshake for the next launch on this stream
-  c->arrive = 0;
-  c->done = 0;
-  c->plan_flag = 0;
-  __threadfence();
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(&d);
+  for (int i = 0; i < 8; ++i) sh.desc[i] = w[i];
+  tf_capture_result& r = c->res;
+  r.capture_seq = c->plan_seq;
+  r.status = status;
+  r.n_rows = (uint32_t)c->plan_rows;
+  r.payload_offset = status == TF_OK ? c->plan_off : 0;
+  r.payload_len = status == TF_OK ? c->plan_bytes : 0;
+  r.skip_before = c->plan_skip;
+  r.ready_seq = d.ready_seq;
+  r.desc = d;
 }
 
 __device__ __forceinline__ const uint8_t* row_src(const CapParams& P, int64_t row) {
@@ -472,8 +452,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   __shared__ CapShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t U = P.units;
+  const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
 
-  // ---- 1. ordered compaction: count kept units, per-thread chunks ----
+  // ---- 1. ordered compaction: count kept units (batch order, no atomics) ----
   int64_t u0 = 0, u1 = 0;
   uint32_t mycnt = 0, mybase = 0;
   uint64_t K;
@@ -499,88 +480,122 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   const uint64_t n_rows = K * (uint64_t)P.rpu;
   if (n_rows == 0) {  // hooks.py:309-311 nothing kept: identity, no descriptor
     if (blockIdx.x == 0 && tid == 0) {
-      st_relaxed_sys(&P.result->payload_len, 0);
-      st_relaxed_sys(&P.result->ready_seq, TF_READY_SENTINEL);
-      st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status), TF_OK);
-      st_release_sys(&P.result->capture_seq, 0);
+      tf_capture_result& r = P.ctl->res;
+      r.capture_seq = 0;
+      r.status = TF_OK;
+      r.n_rows = 0;
+      r.payload_len = 0;
+      r.ready_seq = TF_READY_SENTINEL;
     }
     return;
   }
   const uint64_t out_bytes = n_rows * (uint64_t)P.out_row_bytes;
 
-  // ---- 2. reservation by the first CTA to arrive ----
+  // ---- 2. leader election; reservation runs while the others prefetch ----
+  bool leader = false;
   if (tid == 0) {
     uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
-    if (t == 0) {
+    leader = (t == 0);
+    if (leader) {
+      P.ctl->k_t0 = t_entry;
       leader_reserve(P, out_bytes, n_rows);
       __threadfence();
       st_release_gpu(&P.ctl->plan_flag, 1u);
-    } else {
-      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(32);
     }
-    sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
-    sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+  }
+
+  // ---- 3. this CTA's slice of the output (independent of the offset) ----
+  int64_t items, spr = 1;
+  if constexpr (MODE == MODE_REDUCE) {
+    items = (int64_t)n_rows;
+  } else {
+    spr = (P.words_per_row + kSeg - 1) / kSeg;
+    items = (int64_t)n_rows * spr;
+  }
+  const int64_t chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = imin64(int64_t(blockIdx.x) * chunk, items);
+  const int64_t i1 = imin64(i0 + chunk, items);
+  const int64_t j_lo = i0 / spr;
+  const int64_t r_lo = j_lo / P.rpu;
+  if (P.keep && i0 < i1) {
+    const int64_t r_hi = ((i1 - 1) / spr) / P.rpu;
+    // rank -> unit table for the ranks this CTA touches
+    if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
+      int64_t rank = mybase;
+      for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
+        if (P.keep[u]) {
+          if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
+          ++rank;
+        }
+      }
+    }
   }
   __syncthreads();
+  auto row_of = [&](int64_t j) -> int64_t {
+    int64_t r = j / P.rpu;
+    int64_t sub = j - r * P.rpu;
+    int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
+    return unit * P.rpu + sub;
+  };
 
-  if (sh.status == TF_OK) {
-    uint8_t* dst_base = P.payload + sh.off;
-    // ---- 3. this CTA's slice of the output ----
-    int64_t items, spr = 1;
-    if constexpr (MODE == MODE_REDUCE) {
-      items = (int64_t)n_rows;
-    } else {
-      spr = (P.words_per_row + kSeg - 1) / kSeg;
-      items = (int64_t)n_rows * spr;
-    }
-    const int64_t chunk = (items + gridDim.x - 1) / gridDim.x;
-    const int64_t i0 = imin64(int64_t(blockIdx.x) * chunk, items);
-    const int64_t i1 = imin64(i0 + chunk, items);
-    if (i0 < i1) {
-      const int64_t j_lo = i0 / spr, j_hi = (i1 - 1) / spr;
-      const int64_t r_lo = j_lo / P.rpu, r_hi = j_hi / P.rpu;
-      if (P.keep) {
-        // rank -> unit table for the ranks this CTA touches
-        if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
-          int64_t rank = mybase;
-          for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
-            if (P.keep[u]) {
-              if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
-              ++rank;
-            }
-          }
-        }
-        __syncthreads();
+  if constexpr (MODE == MODE_COPY) {
+    using V = typename VecT<VW>::T;
+    const int64_t wpr = P.words_per_row;
+    // prefetch this warp's first segment before the offset is known
+    int64_t s = i0 + warp;
+    V v[kUnroll];
+    int64_t k0 = 0, k1 = 0, j = 0;
+    if (s < i1) {
+      j = s / spr;
+      k0 = (s - j * spr) * kSeg;
+      k1 = imin64(k0 + kSeg, wpr);
+      const uint8_t* src = row_src(P, row_of(j));
+#pragma unroll
+      for (int i = 0; i < kUnroll; ++i) {
+        int64_t k = k0 + lane + i * 32;
+        if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
       }
-      auto row_of = [&](int64_t j) -> int64_t {
-        int64_t r = j / P.rpu;
-        int64_t sub = j - r * P.rpu;
-        int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
-        return unit * P.rpu + sub;
-      };
-
-      if constexpr (MODE == MODE_COPY) {
-        using V = typename VecT<VW>::T;
-        const int64_t wpr = P.words_per_row;
-        for (int64_t s = i0 + warp; s < i1; s += kWarps) {
-          const int64_t j = s / spr;
-          const int64_t k0 = (s - j * spr) * kSeg;
-          const int64_t k1 = imin64(k0 + kSeg, wpr);
-          const uint8_t* src = row_src(P, row_of(j));
-          uint8_t* dst = dst_base + j * P.out_row_bytes;
-          V v[kUnroll];
+    }
+    if (tid == 0) {
+      if (!leader)
+        while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+      sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
+      sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+    }
+    __syncthreads();
+    if (sh.status == TF_OK && s < i1) {
+      uint8_t* dst_base = P.payload + sh.off;
+      for (;;) {
+        uint8_t* dst = dst_base + j * P.out_row_bytes;
 #pragma unroll
-          for (int i = 0; i < kUnroll; ++i) {
-            int64_t k = k0 + lane + i * 32;
-            if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
-          }
-#pragma unroll
-          for (int i = 0; i < kUnroll; ++i) {
-            int64_t k = k0 + lane + i * 32;
-            if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
-          }
+        for (int i = 0; i < kUnroll; ++i) {
+          int64_t k = k0 + lane + i * 32;
+          if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
         }
-      } else if constexpr (MODE == MODE_CAST) {
+        s += kWarps;
+        if (s >= i1) break;
+        j = s / spr;
+        k0 = (s - j * spr) * kSeg;
+        k1 = imin64(k0 + kSeg, wpr);
+        const uint8_t* src = row_src(P, row_of(j));
+#pragma unroll
+        for (int i = 0; i < kUnroll; ++i) {
+          int64_t k = k0 + lane + i * 32;
+          if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+        }
+      }
+    }
+  } else {
+    if (tid == 0) {
+      if (!leader)
+        while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+      sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
+      sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+    }
+    __syncthreads();
+    if (sh.status == TF_OK && i0 < i1) {
+      uint8_t* dst_base = P.payload + sh.off;
+      if constexpr (MODE == MODE_CAST) {
         // VW == 8: groups of 8 elements; VW == 1: single elements
         constexpr int WI = Elem<IN_DT>::W, WO = Elem<OUT_DT>::W;
         const int64_t wpr = P.words_per_row;
@@ -666,17 +681,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     }
   }
 
-  // ---- 4. last CTA publishes ----
+  // ---- 4. the last CTA to retire publishes ----
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
+    __threadfence();  // this CTA's payload stores, gpu scope, before the count
     uint32_t t = atomicAdd(&P.ctl->done, 1u);
     sh.is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (sh.is_last && tid == 0) {
-    __threadfence();
-    last_cta_publish(P);
+  if (sh.is_last) {
+    if (tid == 0) {
+      __threadfence();
+      last_cta_prepare(P, sh);
+    }
+    __syncthreads();
+    // one coalesced 64-byte post of the descriptor, no system fence: the
+    // host verifies the checksum before it trusts the slot
+    if (sh.publish && warp == 0 && lane < 8) sh.slot[lane] = sh.desc[lane];
+    if (tid == 0) {  // re-arm the handshake for the next launch on this stream
+      P.ctl->arrive = 0;
+      P.ctl->done = 0;
+      P.ctl->plan_flag = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -684,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 // publish rules exposed one call at a time, for the reference's ring tests.
 __global__ void reserve_kernel(CapParams P, uint64_t len) {
   DevCtl* c = P.ctl;
-  uint64_t L = ld_relaxed_sys(&P.cons->L);
+  uint64_t L = ld_relaxed_gpu(&P.dcons->L);
   tf_pstate p = c->p;
   uint64_t off = 0, skip = 0;
   uint32_t kind = 0;
@@ -695,18 +722,16 @@ __global__ void reserve_kernel(CapParams P, uint64_t len) {
     if (kind & TF_DESC_DEAD_SKIP) c->dead_created += skip;
     status = TF_OK;
   }
-  write_mirror(P);
-  st_relaxed_sys(&P.result->payload_offset, off);
-  st_relaxed_sys(&P.result->skip_before, skip);
-  st_relaxed_sys(&P.result->payload_len, len);
-  st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status),
-                 uint64_t(status) | (uint64_t(kind) << 32));
-  __threadfence_system();
+  c->res.status = status;
+  c->res.n_rows = kind;
+  c->res.payload_offset = off;
+  c->res.skip_before = skip;
+  c->res.payload_len = len;
 }
 
 __global__ void publish_kernel(CapParams P, tf_descriptor d) {
   DevCtl* c = P.ctl;
-  uint64_t mtail = ld_relaxed_sys(&P.cons->meta_tail);
+  uint64_t mtail = ld_relaxed_gpu(&P.dcons->meta_tail);
   uint32_t status = TF_OK;
   uint64_t seq = TF_READY_SENTINEL;
   if (c->meta_head - mtail >= P.slots) {
@@ -719,19 +744,17 @@ __global__ void publish_kernel(CapParams P, tf_descriptor d) {
       c->errors |= TF_DEVERR_PROTOCOL;
     } else {
       seq = c->meta_head;
-      d.ready_seq = TF_READY_SENTINEL;
-      const uint64_t* s = reinterpret_cast<const uint64_t*>(&d);
-      __threadfence_system();
+      d.ready_seq = seq;
+      uint64_t* s = reinterpret_cast<uint64_t*>(&d);
+      d.checksum = tf_desc_checksum(s);
       for (int i = 0; i < 8; ++i)
         if (i != 3) st_relaxed_sys(w + i, s[i]);
-      st_release_sys(w + 3, seq);
+      st_relaxed_sys(w + 3, seq);
       c->meta_head = seq + 1;
     }
   }
-  write_mirror(P);
-  st_relaxed_sys(&P.result->ready_seq, seq);
-  st_relaxed_sys(reinterpret_cast<uint64_t*>(&P.result->status), status);
-  __threadfence_system();
+  c->res.ready_seq = seq;
+  c->res.status = status;
 }
 
 }  // namespace
@@ -751,12 +774,19 @@ static CapParams base_params(tf_ring* r) {
   P.cap = r->cfg.payload_capacity;
   P.slots = r->cfg.meta_slots;
   P.meta = r->meta;
-  P.cons = r->cons;
-  P.mirror = r->mirror;
-  P.result = r->result;
+  P.dcons = r->dcons;
   P.ctl = r->ctl;
   P.timeout_ns = r->cfg.wait_timeout_ns ? r->cfg.wait_timeout_ns : 30000000000ull;
   return P;
+}
+
+// Copy the device control block to the pinned snapshot (control stream:
+// never waits for the inference stream). Callers fence the producer first.
+static int snapshot(tf_ring* r) {
+  CUDA_TRY(cudaMemcpyAsync(r->ctl_host, r->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)r->ctrl_stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->ctrl_stream));
+  return TF_OK;
 }
 
 extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** out) {
@@ -780,10 +810,10 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
   auto fail = [&](int code) {
     if (r->payload) cudaFree(r->payload);
     if (r->ctl) cudaFree(r->ctl);
+    if (r->dcons) cudaFree(r->dcons);
     if (r->meta) cudaFreeHost(r->meta);
-    if (r->cons) cudaFreeHost(r->cons);
-    if (r->mirror) cudaFreeHost(r->mirror);
-    if (r->result) cudaFreeHost(r->result);
+    if (r->ctl_host) cudaFreeHost(r->ctl_host);
+    if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
     delete r;
     return code;
   };
@@ -794,31 +824,25 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     cudaGetLastError();
     return fail(TF_ERR_ALLOCATION);  // rings.py:155-160 AllocationError
   }
-  const unsigned hflags = cudaHostAllocMapped | cudaHostAllocPortable;
   size_t meta_bytes = size_t(cfg->meta_slots) * TF_DESCRIPTOR_SIZE;
-  if (cudaHostAlloc((void**)&r->meta, meta_bytes, hflags) != cudaSuccess ||
-      cudaHostAlloc((void**)&r->cons, sizeof(ConsumerShared), hflags) != cudaSuccess ||
-      cudaHostAlloc((void**)&r->mirror, sizeof(ProducerMirror), hflags) != cudaSuccess ||
-      cudaHostAlloc((void**)&r->result, sizeof(tf_capture_result), hflags) != cudaSuccess) {
+  if (cudaHostAlloc((void**)&r->meta, meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable) != cudaSuccess) {
     tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_ALLOCATION);
   }
   memset(r->meta, 0, meta_bytes);
   for (uint32_t s = 0; s < cfg->meta_slots; ++s)  // rings.py:213-215
     reinterpret_cast<uint64_t*>(r->meta + size_t(s) * TF_DESCRIPTOR_SIZE)[3] = TF_READY_SENTINEL;
-  memset(r->cons, 0, sizeof(ConsumerShared));
-  memset(r->mirror, 0, sizeof(ProducerMirror));
-  r->mirror->reset_mark = TF_NO_MARK;
-  memset(r->result, 0, sizeof(tf_capture_result));
-  if (cudaMalloc(&r->ctl, sizeof(DevCtl)) != cudaSuccess) {
+  if (cudaMalloc(&r->ctl, sizeof(DevCtl)) != cudaSuccess ||
+      cudaMalloc(&r->dcons, sizeof(DevConsumer)) != cudaSuccess) {
     tf_set_error("device control block allocation failed");
     cudaGetLastError();
     return fail(TF_ERR_ALLOCATION);
   }
-  DevCtl init;
-  memset(&init, 0, sizeof(init));
-  init.p.reset_mark = TF_NO_MARK;
-  if (cudaMemcpy(r->ctl, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess ||
+  memset(r->ctl_host, 0, sizeof(DevCtl));
+  r->ctl_host->p.reset_mark = TF_NO_MARK;
+  if (cudaMemcpy(r->ctl, r->ctl_host, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(r->dcons, 0, sizeof(DevConsumer)) != cudaSuccess ||
       cudaMemset(r->payload, 0, cfg->payload_capacity) != cudaSuccess) {
     tf_set_error("device init failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_CUDA);
@@ -828,7 +852,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     tf_set_error("stream create failed");
     return fail(TF_ERR_CUDA);
   }
-  r->own_stream = s;
+  r->ctrl_stream = s;
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TF_ERR_CUDA);
   *out = r;
   return TF_OK;
@@ -838,13 +862,12 @@ extern "C" int tf_ring_destroy(tf_ring* r) {
   if (!r) return TF_OK;
   cudaSetDevice(r->device);
   cudaDeviceSynchronize();
-  if (r->own_stream) cudaStreamDestroy((cudaStream_t)r->own_stream);
+  if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
   cudaFree(r->payload);
   cudaFree(r->ctl);
+  cudaFree(r->dcons);
   cudaFreeHost(r->meta);
-  cudaFreeHost(r->cons);
-  cudaFreeHost(r->mirror);
-  cudaFreeHost(r->result);
+  cudaFreeHost(r->ctl_host);
   delete r;
   return TF_OK;
 }
@@ -981,6 +1004,8 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (a->mid > 1) sal = std::min(sal, pow2_align((uint64_t)a->stride_mid));
   const int64_t total_rows = a->outer * a->mid;
   const uint64_t out_max = uint64_t(total_rows) * uint64_t(orb);
+  // grid: one 16 KiB chunk per CTA up to kCtasPerSm CTAs per SM (all
+  // resident, so the spin on the leader's plan can never starve it)
   int grid_bytes = int(std::min<uint64_t>((out_max + (16u << 10) - 1) / (16u << 10),
                                           uint64_t(g_sm_count) * kCtasPerSm));
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
@@ -1031,9 +1056,11 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
 
 extern "C" int tf_ring_last_result(tf_ring* r, tf_capture_result* out) {
   if (!r || !out) return TF_ERR_VALUE;
-  memcpy(out, (const void*)r->result, sizeof(*out));
-  out->status = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) & 0xFFFFFFFFu);
-  out->n_rows = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) >> 32);
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  rc = snapshot(r);
+  if (rc) return rc;
+  *out = r->ctl_host->res;
   return TF_OK;
 }
 
@@ -1046,21 +1073,23 @@ extern "C" int tf_ring_reserve(tf_ring* r, void* stream, uint64_t length,
   if (length > r->cfg.payload_capacity) { tf_set_error("reservation exceeds payload capacity"); return TF_ERR_VALUE; }
   int rc = set_device(r->device);
   if (rc) return rc;
-  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (CUDA convention)
+  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->ctrl_stream));
   CapParams P = base_params(r);
   reserve_kernel<<<1, 1, 0, s>>>(P, length);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s));
-  uint64_t st = *reinterpret_cast<volatile uint64_t*>(&r->result->status);
-  uint32_t status = uint32_t(st & 0xFFFFFFFFu), kind = uint32_t(st >> 32);
-  if (status != TF_OK) {
+  rc = snapshot(r);
+  if (rc) return rc;
+  const tf_capture_result& res = r->ctl_host->res;
+  if (res.status != TF_OK) {
     tf_set_error("need %llu bytes", (unsigned long long)length);
     return TF_ERR_PAYLOAD_RING_FULL;
   }
-  uint64_t off = r->result->payload_offset, skip = r->result->skip_before;
+  uint64_t off = res.payload_offset, skip = res.skip_before;
   {
     std::lock_guard<std::mutex> g(r->mu);
-    HostRegion hr{off, length, skip, kind};
+    HostRegion hr{off, length, skip, res.n_rows /* kind */};
     r->regions.push_back(hr);
     r->host_reserved[off] = hr;
   }
@@ -1074,7 +1103,7 @@ extern "C" int tf_ring_publish(tf_ring* r, void* stream, const tf_descriptor* d,
   if (!r || !d) return TF_ERR_VALUE;
   int rc = set_device(r->device);
   if (rc) return rc;
-  cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (CUDA convention)
+  cudaStream_t s = (cudaStream_t)stream;
   tf_descriptor dd = *d;
   if (dd.capture_seq == 0) {
     // user-built descriptor for a tf_ring_reserve'd region: its region is
@@ -1087,24 +1116,27 @@ extern "C" int tf_ring_publish(tf_ring* r, void* stream, const tf_descriptor* d,
     }
     dd.flags |= TF_DESC_HOST_RESERVED;
   }
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->ctrl_stream));
   CapParams P = base_params(r);
   publish_kernel<<<1, 1, 0, s>>>(P, dd);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s));
-  uint32_t status = uint32_t(*reinterpret_cast<volatile uint64_t*>(&r->result->status) & 0xFFFFFFFFu);
-  if (status == TF_ERR_META_RING_FULL) {
+  rc = snapshot(r);
+  if (rc) return rc;
+  const tf_capture_result& res = r->ctl_host->res;
+  if (res.status == TF_ERR_META_RING_FULL) {
     tf_set_error("all %u descriptor slots are in flight", r->cfg.meta_slots);
-    return status;
+    return TF_ERR_META_RING_FULL;
   }
-  if (status == TF_ERR_PROTOCOL) {
+  if (res.status == TF_ERR_PROTOCOL) {
     tf_set_error("descriptor slot reused before consumption");
-    return status;
+    return TF_ERR_PROTOCOL;
   }
   if (dd.capture_seq == 0) {
     std::lock_guard<std::mutex> g(r->mu);
     r->host_reserved.erase(dd.payload_offset);
   }
-  if (ready_seq) *ready_seq = r->result->ready_seq;
+  if (ready_seq) *ready_seq = res.ready_seq;
   return TF_OK;
 }
 
@@ -1116,22 +1148,86 @@ static inline uint64_t slot_ready(const tf_ring* r, uint64_t slot) {
   return __atomic_load_n(p, __ATOMIC_ACQUIRE);
 }
 
+// Stream-ordered u64 write into device memory: cuStreamWriteValue64 via
+// the driver entry point (the value rides in the command, no host buffer);
+// a pinned-slot cudaMemcpyAsync if stream memory ops are unavailable.
+typedef int (*write64_fn)(void*, unsigned long long, unsigned long long, unsigned int);
+static write64_fn g_write64 = nullptr;
+static int g_write64_probe = 0;
+static std::mutex g_slot_mu;
+static uint64_t* g_slots = nullptr;
+static uint64_t g_slot_next = 0;
+constexpr uint64_t kSlots = 1u << 16;
+
+int tf_internal_write_u64(void* stream, uint64_t* dev_addr, uint64_t value) {
+  if (!g_write64_probe) {
+    std::lock_guard<std::mutex> g(g_slot_mu);
+    if (!g_write64_probe) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess && fn) {
+        int dev = 0, ok = 0;
+        cudaGetDevice(&dev);
+        void* attr = nullptr;
+        cudaDriverEntryPointQueryResult q2;
+        if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &attr, cudaEnableDefault, &q2) == cudaSuccess && attr) {
+          typedef int (*attr_fn)(int*, int, int);
+          ((attr_fn)attr)(&ok, 122 /* CAN_USE_64_BIT_STREAM_MEM_OPS */, dev);
+        }
+        if (ok && !getenv("TF_NO_STREAM_MEMOPS")) g_write64 = (write64_fn)fn;
+      }
+      cudaGetLastError();
+      g_write64_probe = 1;
+    }
+  }
+  if (g_write64) {
+    int rc = g_write64(stream, (unsigned long long)(uintptr_t)dev_addr, value, 0);
+    if (rc != 0) {
+      tf_set_error("cuStreamWriteValue64 failed (%d)", rc);
+      return TF_ERR_CUDA;
+    }
+    return TF_OK;
+  }
+  uint64_t* slot;
+  {
+    std::lock_guard<std::mutex> g(g_slot_mu);
+    if (!g_slots && cudaHostAlloc((void**)&g_slots, kSlots * 8, cudaHostAllocPortable) != cudaSuccess) {
+      tf_set_error("pinned slot allocation failed");
+      return TF_ERR_ALLOCATION;
+    }
+    slot = &g_slots[g_slot_next++ % kSlots];
+  }
+  *slot = value;
+  CUDA_TRY(cudaMemcpyAsync(dev_addr, slot, 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return TF_OK;
+}
+
+static bool slot_verified(const uint8_t* raw, tf_descriptor* d) {
+  uint64_t w[8];
+  memcpy(w, raw, 64);
+  if (w[3] == TF_READY_SENTINEL || tf_desc_checksum(w) != w[7]) return false;
+  memcpy(d, w, 64);
+  return true;
+}
+
 int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
                      uint32_t* n, bool consume) {
   uint32_t got = 0;
   const uint64_t slots = r->cfg.meta_slots;
   uint64_t tail = r->meta_tail;
+  bool advanced = false;
   while (got < max_entries && got < slots) {
     uint64_t slot = tail % slots;
     uint64_t ready = slot_ready(r, slot);
     if (ready == TF_READY_SENTINEL) break;
     tf_descriptor d;
-    memcpy(&d, r->meta + slot * TF_DESCRIPTOR_SIZE, sizeof(d));
-    d.ready_seq = ready;
+    // words may still be landing: accept only a slot whose checksum verifies
+    if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, &d)) break;
     if (consume) {
-      if (ready != r->consumed) {  // rings.py:397-401
+      if (d.ready_seq != r->consumed) {  // rings.py:397-401
         tf_set_error("descriptor sequence %llu out of order, expected %llu",
-                     (unsigned long long)ready, (unsigned long long)r->consumed);
+                     (unsigned long long)d.ready_seq, (unsigned long long)r->consumed);
         *n = got;
         return TF_ERR_PROTOCOL;
       }
@@ -1139,7 +1235,7 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
       __atomic_store_n(rp, TF_READY_SENTINEL, __ATOMIC_RELEASE);
       r->meta_tail = ++tail;
       r->consumed += 1;
-      __atomic_store_n(&r->cons->meta_tail, r->meta_tail, __ATOMIC_RELEASE);
+      advanced = true;
       if (!(d.flags & TF_DESC_HOST_RESERVED))
         r->regions.push_back(HostRegion{d.payload_offset, tf_round_up16(d.payload_len),
                                         d.skip_before, d.flags});
@@ -1150,6 +1246,8 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
     ++got;
   }
   *n = got;
+  if (advanced)  // slots are free once consumed (rings.py:402-404)
+    return tf_internal_write_u64(r->ctrl_stream, &r->dcons->meta_tail, r->meta_tail);
   return TF_OK;
 }
 
@@ -1169,8 +1267,11 @@ extern "C" int tf_ring_ready_bytes(tf_ring* r, uint64_t* n) {
   const uint64_t slots = r->cfg.meta_slots;
   for (uint64_t i = 0; i < slots; ++i) {
     uint64_t slot = (r->meta_tail + i) % slots;
-    if (slot_ready(r, slot) == TF_READY_SENTINEL) break;
-    total += reinterpret_cast<const uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE)[1];
+    tf_descriptor d;
+    if (slot_ready(r, slot) == TF_READY_SENTINEL ||
+        !slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, &d))
+      break;
+    total += d.payload_len;
   }
   *n = total;
   return TF_OK;
@@ -1188,8 +1289,7 @@ extern "C" int tf_ring_poll_ready(tf_ring* r, uint32_t max_entries, tf_descripto
   return tf_internal_poll(r, max_entries, out, n, true);
 }
 
-extern "C" int tf_ring_release_payload(tf_ring* r, uint64_t offset, uint64_t length) {
-  if (!r) return TF_ERR_VALUE;
+int tf_internal_release(tf_ring* r, uint64_t offset, uint64_t length, bool push) {
   std::lock_guard<std::mutex> g(r->mu);
   if (r->regions.empty()) {  // rings.py:420-421
     tf_set_error("no outstanding reservation to release");
@@ -1202,59 +1302,81 @@ extern "C" int tf_ring_release_payload(tf_ring* r, uint64_t offset, uint64_t len
                  (unsigned long long)h.off, (unsigned long long)h.len);
     return TF_ERR_OUT_OF_ORDER_RELEASE;
   }
-  if (h.kind & TF_DESC_DEAD_SKIP) r->dead_reclaimed += h.skip;
+  if (h.kind & TF_DESC_DEAD_SKIP) r->dead_reclaimed += h.skip;  // :415-419
   r->L += h.skip + h.len;
   r->bytes_released += h.len;
   r->host_reserved.erase(h.off);
   r->regions.pop_front();
-  __atomic_store_n(&r->cons->L, r->L, __ATOMIC_RELEASE);
+  if (push) return tf_internal_write_u64(r->ctrl_stream, &r->dcons->L, r->L);
   return TF_OK;
 }
 
-static void producer_snapshot(const tf_ring* r, tf_pstate* p, uint64_t* meta_head) {
-  const volatile ProducerMirror* m = r->mirror;
-  p->V = m->V;
-  p->reset_mark = m->reset_mark;
-  p->reset_credit = m->reset_credit;
-  *meta_head = m->meta_head;
+uint64_t tf_internal_l_after_all(tf_ring* r) {
+  std::lock_guard<std::mutex> g(r->mu);
+  uint64_t L = r->L;
+  for (const HostRegion& h : r->regions) L += h.skip + h.len;
+  return L;
 }
 
+extern "C" int tf_ring_release_payload(tf_ring* r, uint64_t offset, uint64_t length) {
+  if (!r) return TF_ERR_VALUE;
+  return tf_internal_release(r, offset, length, true);
+}
+
+extern "C" int tf_ring_sync_consumer(tf_ring* r) {
+  if (!r) return TF_ERR_VALUE;
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->ctrl_stream));
+  return TF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// shared: snapshots (rings.py:241-276)
+// ---------------------------------------------------------------------------
 extern "C" int tf_ring_get_state(tf_ring* r, tf_ring_state* o) {
   if (!r || !o) return TF_ERR_VALUE;
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  rc = snapshot(r);
+  if (rc) return rc;
   std::lock_guard<std::mutex> g(r->mu);
-  tf_pstate p;
-  uint64_t mh;
-  producer_snapshot(r, &p, &mh);
+  const DevCtl* c = r->ctl_host;
   const uint64_t cap = r->cfg.payload_capacity;
-  const volatile ProducerMirror* m = r->mirror;
   memset(o, 0, sizeof(*o));
-  o->payload_head = tf_head(&p, cap);
-  o->payload_tail = tf_tail(&p, r->L, cap);
-  o->occupancy = tf_used(&p, r->L);
+  o->payload_head = tf_head(&c->p, cap);
+  o->payload_tail = tf_tail(&c->p, r->L, cap);
+  o->occupancy = tf_used(&c->p, r->L);
   o->payload_capacity = cap;
-  o->meta_head = mh;
+  o->meta_head = c->meta_head;
   o->meta_tail = r->meta_tail;
   o->meta_slots = r->cfg.meta_slots;
   o->high_watermark = r->cfg.high_watermark;
-  o->bytes_reserved = m->bytes_reserved;
+  o->bytes_reserved = c->bytes_reserved;
   o->bytes_released = r->bytes_released;
-  o->dead_created = m->dead_created;
+  o->dead_created = c->dead_created;
   o->dead_reclaimed = r->dead_reclaimed;
-  o->descriptors_published = mh;
+  o->descriptors_published = c->meta_head;
   o->descriptors_consumed = r->consumed;
-  o->captures_launched = m->captures;
-  o->drops = m->drops;
-  o->drop_bytes = m->drop_bytes;
-  o->stall_events = m->stall_events;
-  o->stall_ns = m->stall_ns;
-  o->device_errors = m->errors;
+  o->captures_launched = c->captures;
+  o->drops = c->drops;
+  o->drop_bytes = c->drop_bytes;
+  o->stall_events = c->stall_events;
+  o->stall_ns = c->stall_ns;
+  o->device_errors = c->errors;
+  o->kernel_ns = c->kernel_ns;
+  o->last_kernel_ns = c->last_kernel_ns;
   return TF_OK;
 }
 
 extern "C" int tf_ring_free_meta_slots(tf_ring* r, uint64_t* n) {
   if (!r || !n) return TF_ERR_VALUE;
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  rc = snapshot(r);
+  if (rc) return rc;
   std::lock_guard<std::mutex> g(r->mu);
-  *n = r->cfg.meta_slots - (r->mirror->meta_head - r->meta_tail);
+  *n = r->cfg.meta_slots - (r->ctl_host->meta_head - r->meta_tail);
   return TF_OK;
 }
 
@@ -1262,17 +1384,20 @@ extern "C" int tf_ring_free_meta_slots(tf_ring* r, uint64_t* n) {
 extern "C" int tf_ring_would_fit(tf_ring* r, const uint64_t* lengths, uint32_t n,
                                  int64_t meta_entries, int* fits) {
   if (!r || !fits || (n && !lengths)) return TF_ERR_VALUE;
-  std::lock_guard<std::mutex> g(r->mu);
-  tf_pstate p;
-  uint64_t mh;
-  producer_snapshot(r, &p, &mh);
-  const uint64_t cap = r->cfg.payload_capacity;
   for (uint32_t i = 0; i < n; ++i) {
     if (lengths[i] == 0 || lengths[i] % TF_COPY_UNIT) {
       tf_set_error("lengths must be positive copy-unit multiples");
       return TF_ERR_VALUE;
     }
   }
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  rc = snapshot(r);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(r->mu);
+  tf_pstate p = r->ctl_host->p;
+  const uint64_t mh = r->ctl_host->meta_head;
+  const uint64_t cap = r->cfg.payload_capacity;
   *fits = 0;
   for (uint32_t i = 0; i < n; ++i) {
     uint64_t off, skip;

@@ -1,15 +1,23 @@
 // ring2_internal.h — memory layout of one ring pair (not part of the ABI).
 //
-//   payload ring     cudaMalloc            device-written by capture kernels,
-//                                          read by the staging D2H
-//   meta ring        cudaHostAlloc mapped  64-B descriptors; device writes
-//                                          body then ready_seq, host polls
-//   ConsumerShared   cudaHostAlloc mapped  host-owned release/meta cursors the
-//                                          device reads when it reserves
-//   ProducerMirror   cudaHostAlloc mapped  device-owned cursors mirrored for
-//                                          host snapshots (state/would_fit)
-//   DevCtl           cudaMalloc            device-owned allocator state,
-//                                          counters and per-launch handshake
+//   payload ring     cudaMalloc            written by capture kernels, read by
+//                                          the staging D2H
+//   meta ring        cudaHostAlloc mapped  64-B descriptors; device posts the
+//                                          words (no fence) with a checksum,
+//                                          host polls and verifies
+//   DevConsumer      cudaMalloc            host-owned release/meta cursors as
+//                                          the device sees them; written by
+//                                          stream-ordered cuStreamWriteValue64
+//                                          (after each D2H, on its stream), so
+//                                          the capture kernel never reads host
+//                                          memory across a busy PCIe link
+//   DevCtl           cudaMalloc            allocator state, counters,
+//                                          per-launch CTA handshake, last
+//                                          result; snapshotted by a D2H copy
+//                                          on the ring's control stream
+//
+// The only host-memory traffic of a capture kernel is the one coalesced
+// 64-byte descriptor store of its last CTA.
 #pragma once
 #include <stdint.h>
 
@@ -19,17 +27,11 @@
 
 #include "ring2_core.h"
 
-struct alignas(64) ConsumerShared {
+struct alignas(128) DevConsumer {
   uint64_t L;          // virtual release cursor (ring2_core.h)
+  uint64_t pad0[15];
   uint64_t meta_tail;  // descriptors consumed
-  uint64_t pad[6];
-};
-
-struct alignas(64) ProducerMirror {
-  uint64_t V, reset_mark, reset_credit, meta_head;
-  uint64_t bytes_reserved, dead_created, captures, drops;
-  uint64_t drop_bytes, stall_events, stall_ns, errors;
-  uint64_t capture_seq, pad[3];
+  uint64_t pad1[15];
 };
 
 struct alignas(128) DevCtl {
@@ -44,7 +46,12 @@ struct alignas(128) DevCtl {
   uint32_t arrive, done, plan_flag, plan_status;
   uint64_t plan_off, plan_skip, plan_len, plan_bytes, plan_rows, plan_seq;
   uint32_t plan_kind, pad0;
-  uint64_t pad1[4];
+  // device-side timing of capture kernels (globaltimer, ns)
+  uint64_t k_t0, kernel_ns, last_kernel_ns;
+  uint64_t pad1;
+  // result of the most recent launch (device memory; the host copies the
+  // whole block on a side stream when it needs a snapshot)
+  tf_capture_result res;
 };
 
 struct HostRegion {
@@ -57,11 +64,10 @@ struct tf_ring {
   tf_ring_config cfg{};
   uint8_t* payload = nullptr;     // device
   uint8_t* meta = nullptr;        // host pinned mapped (device alias == same VA)
-  ConsumerShared* cons = nullptr; // host pinned mapped
-  ProducerMirror* mirror = nullptr;
-  tf_capture_result* result = nullptr;
+  DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
-  void* own_stream = nullptr;     // cudaStream_t used when the caller passes NULL
+  DevCtl* ctl_host = nullptr;     // pinned snapshot target
+  void* ctrl_stream = nullptr;    // cudaStream_t for consumer-cursor updates
   // consumer-role state (host)
   std::mutex mu;
   uint64_t L = 0, meta_tail = 0, consumed = 0;
@@ -73,4 +79,26 @@ struct tf_ring {
 // cross-TU helpers (ring2.cu)
 int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
                      uint32_t* n, bool consume);
+// release without pushing L to the device (the staging stream already
+// wrote it behind the D2H)
+int tf_internal_release(tf_ring* r, uint64_t offset, uint64_t length, bool push);
+// L after releasing every region currently queued on the host
+uint64_t tf_internal_l_after_all(tf_ring* r);
+// stream-ordered write of one u64 into device memory
+int tf_internal_write_u64(void* stream, uint64_t* dev_addr, uint64_t value);
 void tf_set_error(const char* fmt, ...);
+
+// descriptor checksum (word 7): the host accepts a slot only when the
+// words it read hash to it, so publication needs no system-scope fence
+TF_HD uint64_t tf_desc_mix(uint64_t h, uint64_t v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  h ^= h >> 31;
+  h *= 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 29;
+  return h;
+}
+TF_HD uint64_t tf_desc_checksum(const uint64_t* w) {
+  uint64_t h = 0x5EED2605ull;
+  for (int i = 0; i < 7; ++i) h = tf_desc_mix(h, w[i]);
+  return h | 1ull;  // never 0 (a zeroed slot never verifies)
+}

@@ -264,7 +264,8 @@ struct tf_stager {
   std::atomic<bool> running{false};
   std::atomic<bool> stop_req{false};
   std::atomic<int> flush_req{0};
-  std::thread drain_th, stage_th;
+  std::thread drain_th, completion_th, stage_th;
+  std::atomic<bool> drain_done{false}, completion_done{false};
   std::deque<Batch*> inflight;
   std::deque<Batch*> to_stage;
   std::deque<tf_paged_batch> out_q;
@@ -282,7 +283,7 @@ static cudaEvent_t take_event(tf_stager* st) {
     return e;
   }
   cudaEvent_t e = nullptr;
-  cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&e, cudaEventBlockingSync);
   return e;
 }
 
@@ -520,6 +521,12 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
       }
     }
   }
+  // Free the regions for the device producer as soon as the copy is done:
+  // a stream-ordered write of the release cursor right behind the D2H, so
+  // the capture kernel sees space without a host round trip.
+  int wrc = tf_internal_write_u64(st->stream, &st->ring->dcons->L,
+                                  tf_internal_l_after_all(st->ring));
+  if (wrc) return wrc;
   cudaEventRecord(bt->ev1, st->stream);
   st->batches[bt->id] = bt;
   st->stats.batches_drained += 1;
@@ -613,7 +620,7 @@ extern "C" int tf_stager_transfer_seconds(tf_stager* st, uint64_t id, double* se
 static int release_batch(tf_stager* st, Batch* b) {
   if (b->released) return TF_OK;
   for (auto& d : b->descs) {
-    int rc = tf_ring_release_payload(st->ring, d.payload_offset, tf_round_up16(d.payload_len));
+    int rc = tf_internal_release(st->ring, d.payload_offset, tf_round_up16(d.payload_len), false);
     if (rc) return rc;
   }
   b->released = true;
@@ -721,41 +728,10 @@ static void drain_loop(tf_stager* st) {
   std::vector<tf_descriptor> tmp;
   std::deque<double> seen;  // observation times of ready entries (max_wait)
   int idle = 0;
-  for (;;) {
+  // Only host-memory polling and D2H issue here: no CUDA query calls in the
+  // spin (they contend with the inference thread's launches in the driver).
+  while (!st->stop_req.load()) {
     bool did = false;
-    const bool stopping = st->stop_req.load();
-    {
-      std::unique_lock<std::mutex> g(st->mu);
-      // 1. completions in issue order
-      while (!st->inflight.empty()) {
-        Batch* b = st->inflight.front();
-        cudaError_t q = cudaEventQuery(b->ev1);
-        if (q == cudaErrorNotReady) break;
-        if (q != cudaSuccess) {
-          tf_set_error("D2H failed: %s", cudaGetErrorString(q));
-          g.unlock();
-          set_bg_error(st, TF_ERR_CUDA);
-          return;
-        }
-        int rc = wait_transfer(st, b);
-        if (!rc) rc = release_batch(st, b);
-        if (rc) {
-          g.unlock();
-          set_bg_error(st, rc);
-          return;
-        }
-        st->inflight.pop_front();
-        st->to_stage.push_back(b);
-        did = true;
-      }
-      if (did) st->cv.notify_all();
-    }
-    if (stopping) {
-      std::lock_guard<std::mutex> g(st->mu);
-      if (st->inflight.empty()) return;
-      continue;
-    }
-    // 2. observe the ready window
     uint32_t n = 0;
     uint64_t bytes = 0;
     ready_summary(st, tmp, &n, &bytes);
@@ -774,12 +750,13 @@ static void drain_loop(tf_stager* st) {
         if (rc) {
           g.unlock();
           set_bg_error(st, rc);
-          return;
+          break;
         }
         if (b) {
           size_t k = std::min(seen.size(), b->descs.size());
           seen.erase(seen.begin(), seen.begin() + k);
           st->inflight.push_back(b);
+          st->cv.notify_all();
           did = true;
         }
       }
@@ -792,6 +769,44 @@ static void drain_loop(tf_stager* st) {
       std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   }
+  st->drain_done = true;
+  st->cv.notify_all();
+}
+
+// Completion: block on the oldest D2H (blocking-sync event, the thread
+// sleeps in the driver), then release its regions and hand it to staging.
+static void completion_loop(tf_stager* st) {
+  bind_thread(st->cpus);
+  cudaSetDevice(st->device);
+  for (;;) {
+    Batch* b = nullptr;
+    {
+      std::unique_lock<std::mutex> g(st->mu);
+      st->cv.wait(g, [&] { return !st->inflight.empty() || st->drain_done.load() || st->bg_error; });
+      if (st->inflight.empty()) break;
+      b = st->inflight.front();
+    }
+    cudaError_t e = cudaEventSynchronize(b->ev1);
+    std::unique_lock<std::mutex> g(st->mu);
+    if (e != cudaSuccess) {
+      tf_set_error("D2H failed: %s", cudaGetErrorString(e));
+      g.unlock();
+      set_bg_error(st, TF_ERR_CUDA);
+      break;
+    }
+    int rc = wait_transfer(st, b);
+    if (!rc) rc = release_batch(st, b);
+    if (rc) {
+      g.unlock();
+      set_bg_error(st, rc);
+      break;
+    }
+    st->inflight.pop_front();
+    st->to_stage.push_back(b);
+    st->cv.notify_all();
+  }
+  st->completion_done = true;
+  st->cv.notify_all();
 }
 
 static void stage_loop(tf_stager* st) {
@@ -801,7 +816,7 @@ static void stage_loop(tf_stager* st) {
     uint8_t* dst = nullptr;
     {
       std::unique_lock<std::mutex> g(st->mu);
-      st->cv.wait(g, [&] { return !st->to_stage.empty() || (st->stop_req && st->inflight.empty()) || st->bg_error; });
+      st->cv.wait(g, [&] { return !st->to_stage.empty() || st->completion_done.load() || st->bg_error; });
       if (st->to_stage.empty()) return;
       b = st->to_stage.front();
       st->to_stage.pop_front();
@@ -862,7 +877,10 @@ extern "C" int tf_stager_start(tf_stager* st) {
   unsigned nthreads = st->cfg.stage_threads ? st->cfg.stage_threads : 3;
   st->copy_pool.start((int)nthreads, st->cpus);
   st->running = true;
+  st->drain_done = false;
+  st->completion_done = false;
   st->drain_th = std::thread(drain_loop, st);
+  st->completion_th = std::thread(completion_loop, st);
   st->stage_th = std::thread(stage_loop, st);
   return TF_OK;
 }
@@ -873,6 +891,8 @@ extern "C" int tf_stager_stop(tf_stager* st) {
   st->stop_req = true;
   st->cv.notify_all();
   if (st->drain_th.joinable()) st->drain_th.join();
+  st->cv.notify_all();
+  if (st->completion_th.joinable()) st->completion_th.join();
   st->cv.notify_all();
   if (st->stage_th.joinable()) st->stage_th.join();
   st->copy_pool.stop();

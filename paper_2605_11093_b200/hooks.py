@@ -434,6 +434,7 @@ def capture(
                         defer_publish=defer_publish)
     s = stream if stream is not None else t.cuda.current_stream(ring.device)
     ring.sync()
+    ring.sync_consumer()   # reserve against the consumer's latest releases
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     e0.record(s)
     launch_capture(ring, args, s)

@@ -139,6 +139,7 @@ class RingState:
     stall_ns: int = 0
     device_errors: int = 0
     captures_launched: int = 0
+    kernel_ns: int = 0
 
     @property
     def free_bytes(self) -> int:
@@ -270,6 +271,10 @@ class RingPair:
         if ev is not None:
             ev.synchronize()
 
+    def sync_consumer(self) -> None:
+        """Wait until the device sees every release/poll made so far."""
+        N.check(N.lib().tf_ring_sync_consumer(self.handle))
+
     # -- shared --------------------------------------------------------------
 
     @property
@@ -296,7 +301,7 @@ class RingPair:
             drops=s.drops, drop_bytes=s.drop_bytes,
             stall_events=s.stall_events, stall_ns=s.stall_ns,
             device_errors=s.device_errors,
-            captures_launched=s.captures_launched)
+            captures_launched=s.captures_launched, kernel_ns=s.kernel_ns)
 
     def counters(self) -> dict:
         s = self._cstate()
