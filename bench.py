@@ -370,8 +370,9 @@ def leg_e2e(args, dist, dev):
 def leg_model(args, dist, dev):
     import torch
 
-    from paper_2605_11093_b200 import (DrainConfig, NullSink, PolicyConfig,
-                                       RingConfig, StepRequest)
+    from paper_2605_11093_b200 import (BEST_EFFORT, DROP_RECENT, DrainConfig,
+                                       NullSink, PolicyConfig, RingConfig,
+                                       StepRequest)
     from paper_2605_11093_b200.hookpoint import Observer
     from paper_2605_11093_b200.integrations import (attach_llama, detach,
                                                     llama3_8b_config,
@@ -389,9 +390,10 @@ def leg_model(args, dist, dev):
     def fwd():
         model.model(input_ids=ids, use_cache=False)
 
-    def make_graph():
-        """Prefill step as one CUDA graph (HookPoints, if attached and the
-        observer is active, are recorded into it)."""
+    def make_graph(obs=None):
+        """Prefill step as one CUDA graph; with an observer, its enabled
+        HookPoints are recorded into the graph (warm-up passes capture
+        nothing: the observer is inactive outside a step)."""
         cs = torch.cuda.Stream(device=dev)
         cs.wait_stream(stream)
         with torch.cuda.stream(cs):
@@ -399,8 +401,13 @@ def leg_model(args, dist, dev):
                 fwd()
         stream.wait_stream(cs)
         graph = torch.cuda.CUDAGraph()
-        with torch.inference_mode(), torch.cuda.graph(graph):
-            model.model(input_ids=ids, use_cache=False)
+        if obs is None:
+            with torch.inference_mode(), torch.cuda.graph(graph):
+                model.model(input_ids=ids, use_cache=False)
+        else:
+            with obs.graph_capture(), torch.inference_mode(), \
+                    torch.cuda.graph(graph):
+                model.model(input_ids=ids, use_cache=False)
         return graph
 
     def run(n, step_fn, obs=None, base=0):
@@ -411,13 +418,17 @@ def leg_model(args, dist, dev):
         a.record(stream)
         for s in range(n):
             if obs is not None:
-                obs.begin_step(batch, base + s)
+                plan = obs.begin_step(batch, base + s)
+                tally["kept"] += len(plan.kept_ids)
+                tally["dropped"] += len(plan.dropped_ids)
             step_fn()
             if obs is not None:
                 obs.end_step(stream)
         b.record(stream)
         b.synchronize()
         return a.elapsed_time(b) / n
+
+    tally = {"kept": 0, "dropped": 0}
 
     n = max(3, args.steps)
     results = {}
@@ -429,8 +440,12 @@ def leg_model(args, dist, dev):
         run(2, step0)
         base = run(n, step0)
         res = {"no_capture_ms": base}
-        for label, sites in (("resid", ("resid_post",)),
-                             ("resid_mlp", ("mlp_act", "resid_post"))):
+        cases = [("resid", ("resid_post",), PolicyConfig()),
+                 ("resid_mlp", ("mlp_act", "resid_post"), PolicyConfig())]
+        if mode == "graph":  # overload regime under the best-effort policy
+            cases.append(("resid_mlp_best_effort", ("mlp_act", "resid_post"),
+                          PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT)))
+        for label, sites, policy in cases:
             reg = llama_registry(cfg, sites)
             step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
             sink = NullSink()
@@ -440,23 +455,25 @@ def leg_model(args, dist, dev):
                                              staging_buffer_size=128 << 20,
                                              staging_buffer_count=6,
                                              mode=args.staging, stage_threads=4),
-                           policy=PolicyConfig(), sink=sink, device=dev.index,
+                           policy=policy, sink=sink, device=dev.index,
                            max_batch=B)
             obs.exporter.copy_payloads = False
             obs.start()
             handles = attach_llama(model, obs, sites)
+            kept0 = dropped0 = 0
             if mode == "graph":
-                obs.begin_step(batch, 0)   # active while recording the graph
-                g1 = make_graph()
-                obs.end_step(stream)
+                g1 = make_graph(obs)
                 step1 = g1.replay
             else:
                 g1, step1 = None, fwd
             obs.flush(300)
             run(max(1, args.warmup - 1), step1, obs, 100)
             obs.flush(300)
+            tally["kept"] = tally["dropped"] = 0
             t = run(n, step1, obs, 1000)   # run time stops at inference end
+            t_tail = time.perf_counter()
             obs.flush(600)                 # export tail, reported apart
+            t_tail = time.perf_counter() - t_tail
             st = obs.ring.state()
             obs.check_device()
             detach(handles)
@@ -464,7 +481,11 @@ def leg_model(args, dist, dev):
             del g1
             res[label] = {
                 "capture_ms": t, "overhead_pct": (t - base) / base * 100.0,
-                "step_bytes": step_bytes, "stall_events": st.stall_events,
+                "step_bytes": step_bytes, "policy": policy.mode,
+                "stall_events": st.stall_events,
+                "dropped_request_steps": tally["dropped"],
+                "kept_request_steps": tally["kept"],
+                "export_tail_s": t_tail,
                 "records": sink.records_written}
         del g0
         results[mode] = res

@@ -14,7 +14,7 @@
 #include "../../include/ring2.h"
 
 // rings.py:63-64 round_up_to_copy_unit
-TF_HD uint64_t tf_round_up16(uint64_t n) { return (n + 15u) & ~uint64_t(15); }
+TF_HD uint64_t tf_round_up16(uint64_t n) { return (n + 15u) & ~(uint64_t)15; }
 
 // rings.py:166-193 _plan_reservation. Returns 1 and (offset, dead) when the
 // request fits, else 0. Rules in order: full; empty -> offset 0; wrapped

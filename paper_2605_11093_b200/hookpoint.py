@@ -170,6 +170,25 @@ class Observer:
         self.ring.note_launch(stream)
         self.active = False
 
+    def graph_capture(self):
+        """Context manager for recording a CUDA graph of one step: enabled
+        HookPoints record their capture kernels into the graph. Replay it
+        between begin_step()/end_step(); the keep vector and step sequence
+        are read from the observer's fixed device buffers at replay time.
+        Re-record after a hook-filter change (disabled hooks must vanish
+        from the graph, §3.4)."""
+        obs = self
+
+        class _Rec:
+            def __enter__(self_inner):
+                obs.registry.commit_filter()
+                obs._was_active = obs.active
+                obs.active = True
+
+            def __exit__(self_inner, *exc):
+                obs.active = obs._was_active
+        return _Rec()
+
     def check_device(self) -> None:
         """Raise if the device dropped a capture the plan admitted."""
         st = self.ring.state()
