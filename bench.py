@@ -54,6 +54,11 @@ def parse():
                    choices=["copy-engine", "mapped"])
     p.add_argument("--legs", default="value,e2e,model,cpu")
     p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--page-out", default="handoff",
+                   choices=["copy", "handoff"],
+                   help="exporter page-out for the e2e and model legs")
+    p.add_argument("--pinned-buffers", type=int, default=12,
+                   help="pinned staging buffers of 128 MiB")
     p.add_argument("--profile", action="store_true",
                    help="value leg only, short; for ncu launch lists")
     return p.parse_args()
@@ -312,8 +317,9 @@ def leg_e2e(args, dist, dev):
                    drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
                                      max_wait=1e-4,
                                      staging_buffer_size=128 << 20,
-                                     staging_buffer_count=6, mode=args.staging,
-                                     stage_threads=4),
+                                     staging_buffer_count=args.pinned_buffers,
+                                     mode=args.staging, stage_threads=4,
+                                     page_out=args.page_out),
                    policy=PolicyConfig(), sink=sink, device=dev.index,
                    max_batch=B)
     obs.exporter.copy_payloads = False
@@ -453,8 +459,9 @@ def leg_model(args, dist, dev):
                            drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
                                              max_wait=1e-4,
                                              staging_buffer_size=128 << 20,
-                                             staging_buffer_count=6,
-                                             mode=args.staging, stage_threads=4),
+                                             staging_buffer_count=args.pinned_buffers,
+                                             mode=args.staging, stage_threads=4,
+                                             page_out=args.page_out),
                            policy=policy, sink=sink, device=dev.index,
                            max_batch=B)
             obs.exporter.copy_payloads = False
@@ -620,7 +627,8 @@ def config_block(args):
             "captures_per_step": 2 * LAYERS,
             "bytes_per_step": B * T * (HIDDEN + FFN) * 2 * LAYERS,
             "parallelism": f"replicas x{args.gpus} (no collective)",
-            "staging": args.staging,
+            "staging": args.staging, "page_out": args.page_out,
+            "pinned_pool": f"{args.pinned_buffers} x 128 MiB",
             "l2": "inputs 4.5 GiB/step >> 126 MB L2 (no flush needed)"}
 
 

@@ -238,6 +238,13 @@ int tf_ring_would_fit(tf_ring* ring, const uint64_t* lengths, uint32_t n,
 #define TF_STAGE_COPY_ENGINE 0 /* cudaMemcpyAsync on a side stream, event-fenced */
 #define TF_STAGE_MAPPED 1      /* SM stores into mapped pinned memory */
 
+/* What the page-out stage does with a landed pinned batch. */
+#define TF_PAGE_OUT_COPY 0     /* copy to pageable memory, return the pinned
+                                  buffer first (exporter.py:237-249) */
+#define TF_PAGE_OUT_HANDOFF 1  /* zero-copy: hand the pinned buffer to the
+                                  consumer; it returns on tf_stager_free_paged */
+#define TF_PAGE_OUT_DISCARD 2  /* D2H-only measurement: drop after landing */
+
 typedef struct tf_drain_config {           /* exporter.py:35-51 */
   uint64_t min_ready_entries;
   uint64_t min_ready_bytes;
@@ -249,7 +256,7 @@ typedef struct tf_drain_config {           /* exporter.py:35-51 */
   int32_t numa_node;                       /* -1 = auto from the GPU's PCI node */
   uint32_t stage_queue_slots;              /* exporter.py:32 (0 = 16) */
   uint32_t stage_threads;                  /* pinned->pageable copy threads (0 = auto) */
-  uint32_t discard_paged;                  /* 1: return pinned buffers without paging out (D2H-only measurement) */
+  uint32_t page_out;                       /* TF_PAGE_OUT_* */
 } tf_drain_config;
 
 typedef struct tf_stager tf_stager;
@@ -318,9 +325,11 @@ typedef struct tf_paged_batch {
   uint32_t n_entries;
   uint32_t reason;
   uint64_t bytes_total;
-  void* payload;             /* malloc'd, bytes_total long */
+  void* payload;             /* pageable (copy) or pinned (hand-off), bytes_total long */
   tf_descriptor* descs;      /* malloc'd, n_entries long */
   uint64_t* starts;          /* malloc'd, n_entries long */
+  int32_t pinned_buffer;     /* pool index under TF_PAGE_OUT_HANDOFF, else -1 */
+  uint32_t _pad;
 } tf_paged_batch;
 int tf_stager_next(tf_stager* st, double timeout_s, tf_paged_batch* out);
 /* Return a batch obtained from tf_stager_next (payload back to the pool). */

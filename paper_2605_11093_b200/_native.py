@@ -63,6 +63,7 @@ TF_DTYPE = {"u8": 0, "i8": 1, "f16": 2, "bf16": 3, "f32": 4, "i32": 5,
 
 TF_STAGE_COPY_ENGINE = 0
 TF_STAGE_MAPPED = 1
+TF_PAGE_OUT = {"copy": 0, "handoff": 1, "discard": 2}
 REASONS = {0: "none", 1: "entries", 2: "bytes", 3: "timeout", 4: "flush"}
 
 
@@ -116,7 +117,7 @@ class CDrainConfig(C.Structure):
                 ("staging_buffer_count", C.c_uint64), ("mode", C.c_uint32),
                 ("mapped_ctas", C.c_uint32), ("numa_node", C.c_int32),
                 ("stage_queue_slots", C.c_uint32),
-                ("stage_threads", C.c_uint32), ("discard_paged", C.c_uint32)]
+                ("stage_threads", C.c_uint32), ("page_out", C.c_uint32)]
 
 
 class CBatchInfo(C.Structure):
@@ -142,7 +143,8 @@ class CPagedBatch(C.Structure):
     _fields_ = [("batch_id", C.c_uint64), ("n_entries", C.c_uint32),
                 ("reason", C.c_uint32), ("bytes_total", C.c_uint64),
                 ("payload", C.c_void_p), ("descs", C.POINTER(CDescriptor)),
-                ("starts", u64p)]
+                ("starts", u64p), ("pinned_buffer", C.c_int32),
+                ("_pad", C.c_uint32)]
 
 
 assert C.sizeof(CDescriptor) == 64

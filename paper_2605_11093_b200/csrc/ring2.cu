@@ -303,7 +303,9 @@ __device__ __forceinline__ uint32_t count_nonzero_bytes(uint32_t w) {
 
 // Block-wide exclusive scan of one u32 per thread; returns the exclusive
 // prefix, writes the total to sh.total.
+template <int NWARPS = kWarps>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, CapShared& sh) {
+  constexpr int kWarps = NWARPS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -707,6 +709,217 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk-copy capture (COPY, 16-B aligned rows): global -> smem -> ring
+// with cp.async.bulk. One CTA per SM, kTmaStages x 32 KiB stages. The
+// loads of the first stages are issued before the reservation is known
+// (the source read does not depend on the ring offset), so the leader's
+// allocator round trip hides behind data already in flight.
+// ---------------------------------------------------------------------------
+constexpr int kTmaThreads = 128;
+constexpr int kTmaWarps = kTmaThreads / 32;
+constexpr int kTmaTile = 32 * 1024;
+constexpr int kTmaStages = 6;
+constexpr int kTmaSmem = kTmaTile * kTmaStages;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kTmaThreads, 1) capture_tma_kernel(CapParams P) {
+  extern __shared__ __align__(128) uint8_t tiles[];
+  __shared__ CapShared sh;
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  const int tid = threadIdx.x;
+  const int64_t U = P.units;
+  const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+
+  // ---- 1. ordered compaction (same as capture_kernel) ----
+  int64_t u0 = 0, u1 = 0;
+  uint32_t mycnt = 0, mybase = 0;
+  uint64_t K;
+  if (P.keep) {
+    int64_t per = (U + kTmaThreads - 1) / kTmaThreads;
+    if (P.keep_vec) per = (per + 15) & ~int64_t(15);
+    u0 = imin64(int64_t(tid) * per, U);
+    u1 = imin64(u0 + per, U);
+    int64_t u = u0;
+    if (P.keep_vec) {
+      for (; u + 16 <= u1; u += 16) {
+        uint4 k = *reinterpret_cast<const uint4*>(P.keep + u);
+        mycnt += count_nonzero_bytes(k.x) + count_nonzero_bytes(k.y) +
+                 count_nonzero_bytes(k.z) + count_nonzero_bytes(k.w);
+      }
+    }
+    for (; u < u1; ++u) mycnt += P.keep[u] != 0;
+    mybase = block_exclusive_scan<kTmaWarps>(mycnt, sh);
+    K = sh.total;
+  } else {
+    K = (uint64_t)U;
+  }
+  const uint64_t n_rows = K * (uint64_t)P.rpu;
+  if (n_rows == 0) {
+    if (blockIdx.x == 0 && tid == 0) {
+      tf_capture_result& r = P.ctl->res;
+      r.capture_seq = 0;
+      r.status = TF_OK;
+      r.n_rows = 0;
+      r.payload_len = 0;
+      r.ready_seq = TF_READY_SENTINEL;
+    }
+    return;
+  }
+  const uint64_t row = (uint64_t)P.out_row_bytes;
+  const uint64_t out_bytes = n_rows * row;
+
+  // ---- 2. this CTA's byte range of the output and its rank table ----
+  uint64_t per_cta = (out_bytes + gridDim.x - 1) / gridDim.x;
+  per_cta = (per_cta + 15) & ~uint64_t(15);
+  const uint64_t b0 = min(out_bytes, uint64_t(blockIdx.x) * per_cta);
+  const uint64_t b1 = min(out_bytes, b0 + per_cta);
+  const int64_t r_lo = int64_t(b0 / row) / P.rpu;
+  if (P.keep && b0 < b1) {
+    const int64_t r_hi = int64_t((b1 - 1) / row) / P.rpu;
+    if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
+      int64_t rank = mybase;
+      for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
+        if (P.keep[u]) {
+          if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
+          ++rank;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 3. one thread drives the bulk-copy pipeline ----
+  if (tid == 0) {
+    auto row_of = [&](int64_t j) -> int64_t {
+      int64_t r = j / P.rpu;
+      int64_t sub = j - r * P.rpu;
+      int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
+      return unit * P.rpu + sub;
+    };
+    const uint64_t span = b1 - b0;
+    const int ntiles = int((span + kTmaTile - 1) / kTmaTile);
+    auto issue = [&](int t) {
+      const int st = t % kTmaStages;
+      const uint64_t tb0 = b0 + uint64_t(t) * kTmaTile;
+      const uint64_t tb1 = min(b1, tb0 + kTmaTile);
+      mbar_expect_tx(&full[st], uint32_t(tb1 - tb0));
+      uint8_t* sdst = tiles + st * kTmaTile;
+      uint64_t cur = tb0;
+      while (cur < tb1) {
+        const uint64_t j = cur / row;
+        const uint64_t off = cur - j * row;
+        const uint64_t len = min(row - off, tb1 - cur);
+        bulk_load(sdst + (cur - tb0), row_src(P, row_of((int64_t)j)) + off, uint32_t(len), &full[st]);
+        cur += len;
+      }
+    };
+    const int pre = ntiles < kTmaStages ? ntiles : kTmaStages;
+    for (int t = 0; t < pre; ++t) issue(t);
+
+    // election + reservation after the prefetch is in flight
+    const uint32_t ticket = atomicAdd(&P.ctl->arrive, 1u);
+    if (ticket == 0) {
+      P.ctl->k_t0 = t_entry;
+      leader_reserve(P, out_bytes, n_rows);
+      __threadfence();
+      st_release_gpu(&P.ctl->plan_flag, 1u);
+    } else {
+      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+    }
+    const uint32_t status = *((volatile uint32_t*)&P.ctl->plan_status);
+    uint8_t* dst_base = P.payload + *((volatile uint64_t*)&P.ctl->plan_off);
+    if (status != TF_OK) {
+      // rejected: only drain the prefetches (smem must outlive them)
+      for (int t = 0; t < pre; ++t) mbar_wait(&full[t], 0u);
+    } else {
+      for (int t = 0; t < ntiles; ++t) {
+        const int st = t % kTmaStages;
+        mbar_wait(&full[st], uint32_t((t / kTmaStages) & 1));
+        const uint64_t tb0 = b0 + uint64_t(t) * kTmaTile;
+        const uint64_t tb1 = min(b1, tb0 + kTmaTile);
+        bulk_store(dst_base + tb0, tiles + st * kTmaTile, uint32_t(tb1 - tb0));
+        bulk_commit();
+        // refill the stage of tile t-1 once its store has read the smem
+        const int nt = t - 1 + kTmaStages;
+        if (t >= 1 && nt < ntiles) {
+          bulk_wait_read<1>();
+          issue(nt);
+        }
+      }
+    }
+    bulk_wait_all();  // every tile written before this CTA counts as done
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    sh.status = status;
+  }
+  __syncthreads();
+
+  // ---- 4. the last CTA to retire publishes ----
+  if (tid == 0) {
+    uint32_t t = atomicAdd(&P.ctl->done, 1u);
+    sh.is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (sh.is_last) {
+    if (tid == 0) {
+      __threadfence();
+      last_cta_prepare(P, sh);
+    }
+    __syncthreads();
+    if (sh.publish && tid < 8) sh.slot[tid] = sh.desc[tid];
+    if (tid == 0) {
+      P.ctl->arrive = 0;
+      P.ctl->done = 0;
+      P.ctl->plan_flag = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Protocol-level producer ops (single thread): the same allocator and
 // publish rules exposed one call at a time, for the reference's ring tests.
 __global__ void reserve_kernel(CapParams P, uint64_t len) {
@@ -1016,6 +1229,29 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (a->op == TF_OP_COPY) {
     int vw = std::min<int>(sal, pow2_align((uint64_t)a->row_bytes));
     P.words_per_row = a->row_bytes / vw;
+    static int copy_path = -1;  // 0 = LDG/STG warps, 1 = TMA bulk copies
+    if (copy_path < 0) {
+      const char* e = getenv("TF_COPY_PATH");
+      copy_path = (e && e[0] == 'l') ? 0 : 1;
+    }
+    if (vw == 16 && copy_path == 1) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        CUDA_TRY(cudaFuncSetAttribute(capture_tma_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+        attr_set = true;
+      }
+      int g = int(std::min<uint64_t>((out_max + kTmaTile - 1) / kTmaTile, uint64_t(g_sm_count)));
+      g = std::max(std::max(g, grid_table), 1);
+      if (a->max_ctas) g = std::max(grid_table, std::min<int>(g, (int)a->max_ctas));
+      capture_tma_kernel<<<g, kTmaThreads, kTmaSmem, s>>>(P);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        tf_set_error("capture launch: %s", cudaGetErrorString(e));
+        return TF_ERR_CUDA;
+      }
+      return TF_OK;
+    }
     switch (vw) {
       case 16: return launch<MODE_COPY, 16, 0, 0>(P, grid, s);
       case 8: return launch<MODE_COPY, 8, 0, 0>(P, grid, s);

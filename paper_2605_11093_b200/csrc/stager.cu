@@ -640,8 +640,8 @@ extern "C" int tf_stager_complete_transfer(tf_stager* st, uint64_t id, double* s
   return rc;
 }
 
-static void retire_batch(tf_stager* st, Batch* b) {
-  st->free_bufs.push_back(b->buf);
+static void retire_batch(tf_stager* st, Batch* b, bool return_buffer = true) {
+  if (return_buffer) st->free_bufs.push_back(b->buf);
   st->event_pool.push_back(b->ev0);
   st->event_pool.push_back(b->ev1);
   st->batches.erase(b->id);
@@ -711,10 +711,15 @@ static uint8_t* paged_alloc(tf_stager* st) {  // caller holds st->mu
 }
 
 static void free_paged_batch(tf_stager* st, tf_paged_batch* b, bool to_pool) {
-  if (b->payload) {
+  if (b->pinned_buffer >= 0) {
+    // zero-copy hand-off: the pinned staging buffer goes back to the pool
+    st->free_bufs.push_back((uint32_t)b->pinned_buffer);
+    st->cv.notify_all();
+  } else if (b->payload) {
     if (to_pool) st->paged_pool.push_back((uint8_t*)b->payload);
     else free(b->payload);
   }
+  b->pinned_buffer = -1;
   free(b->descs);
   free(b->starts);
   b->payload = nullptr;
@@ -820,7 +825,7 @@ static void stage_loop(tf_stager* st) {
       if (st->to_stage.empty()) return;
       b = st->to_stage.front();
       st->to_stage.pop_front();
-      if (st->cfg.discard_paged) {
+      if (st->cfg.page_out == TF_PAGE_OUT_DISCARD) {
         // D2H-only measurement: the bytes have landed in the pinned host
         // ring; hand the buffer straight back.
         st->stats.batches_staged += 1;
@@ -828,17 +833,21 @@ static void stage_loop(tf_stager* st) {
         st->cv.notify_all();
         continue;
       }
-      dst = paged_alloc(st);
+      if (st->cfg.page_out == TF_PAGE_OUT_COPY) dst = paged_alloc(st);
     }
-    if (!dst) {
+    const bool handoff = st->cfg.page_out == TF_PAGE_OUT_HANDOFF;
+    if (!handoff && !dst) {
       tf_set_error("pageable allocation failed");
       set_bg_error(st, TF_ERR_ALLOCATION);
       return;
     }
-    // pinned -> pageable (exporter.py:237-249), NUMA-local, parallel
-    st->copy_pool.copy(dst, st->bufs[b->buf], b->bytes);
+    // pinned -> pageable (exporter.py:237-249), NUMA-local, parallel; or
+    // zero-copy hand-off of the pinned buffer itself
+    if (!handoff) st->copy_pool.copy(dst, st->bufs[b->buf], b->bytes);
     tf_paged_batch pb;
     memset(&pb, 0, sizeof(pb));
+    pb.pinned_buffer = handoff ? (int32_t)b->buf : -1;
+    if (handoff) dst = st->bufs[b->buf];
     pb.batch_id = b->id;
     pb.n_entries = (uint32_t)b->descs.size();
     pb.reason = b->reason;
@@ -852,7 +861,7 @@ static void stage_loop(tf_stager* st) {
       std::unique_lock<std::mutex> g(st->mu);
       st->pageable_in_flight += b->bytes;
       st->stats.batches_staged += 1;
-      retire_batch(st, b);  // pinned buffer back before the hand-off
+      retire_batch(st, b, !handoff);  // copy mode: buffer back before the hand-off
       note_transient(st);
       st->cv.notify_all();
       st->cv.wait(g, [&] { return st->out_q.size() < st->cfg.stage_queue_slots || st->stop_req; });

@@ -50,9 +50,20 @@ class DrainConfig:
     numa_node: int = -1
     stage_threads: int = 0
     stage_queue_slots: int = STAGE_QUEUE_SLOTS
-    discard_paged: bool = False   # D2H-only measurement (no page-out / sink)
+    # page-out stage: "copy" = pinned -> pageable then the buffer returns
+    # (the reference's stage_to_pageable); "handoff" = zero-copy, the sink
+    # reads the pinned buffer, which returns when the batch is sunk;
+    # "discard" = D2H-only measurement
+    page_out: str = "copy"
+    discard_paged: bool = False   # alias for page_out="discard"
+
+    @property
+    def page_out_mode(self) -> str:
+        return "discard" if self.discard_paged else self.page_out
 
     def __post_init__(self) -> None:
+        if self.page_out not in N.TF_PAGE_OUT:
+            raise ConfigError(f"unknown page-out mode {self.page_out!r}")
         if min(self.min_ready_entries, self.min_ready_bytes) <= 0:
             raise ConfigError("ready thresholds must be positive")
         if self.max_wait <= 0:
@@ -68,7 +79,7 @@ class DrainConfig:
             self.staging_buffer_size, self.staging_buffer_count,
             STAGING_MODES[self.mode], self.mapped_ctas, self.numa_node,
             self.stage_queue_slots, self.stage_threads,
-            1 if self.discard_paged else 0)
+            N.TF_PAGE_OUT[self.page_out_mode])
 
 
 class StagingBuffer:
@@ -402,7 +413,7 @@ class ExportPipeline:
         """Block until every published capture has been drained and sunk."""
         self._check_bg()
         N.check(N.lib().tf_stager_flush(self._st, timeout))
-        if self.config.discard_paged:
+        if self.config.page_out_mode == "discard":
             return
         deadline = time.monotonic() + timeout
         while True:

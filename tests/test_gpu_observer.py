@@ -1,0 +1,249 @@
+"""End to end through the public API: Observer + HookPoint + policy +
+background export, against the oracle's synchronous reference records
+(criterion 1 of PKG/tests/test_acceptance.py:90-125, now on a GPU), plus
+CUDA-graph replay and a real random-init GPT-2 (BASELINE configs[0])."""
+
+import zlib
+
+import pytest
+import torch
+
+from oracle import workload as W
+from paper_2605_11093_b200 import (BEST_EFFORT, COMPLETENESS, DROP_RECENT,
+                                   DrainConfig, DType, HookSpec, ModelSpec,
+                                   PolicyConfig, RingConfig, StepRequest,
+                                   install_hooks)
+from paper_2605_11093_b200.hookpoint import HookPoint, Observer
+
+pytestmark = pytest.mark.gpu
+
+
+class Collect:
+    def __init__(self):
+        self.records = []
+
+    def write(self, recs):
+        self.records.extend(recs)
+
+
+def _hooks(hidden):
+    return [HookSpec("resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+            HookSpec("logits", ("tokens", 8), DType.of("f32"))]
+
+
+def _run_workload(obs, reg, seed, sched, hidden):
+    """Drive the synthetic schedule: per step plan, then fire every enabled
+    hook with the reference's content bytes for the whole batch."""
+    keep_log = {}
+    for seq, _, batch in sched:
+        reqs = [StepRequest(r.request_id, r.arrival_index, r.prompt, r.tokens,
+                            r.token_start) for r in batch]
+        plan = obs.begin_step(reqs, seq)
+        keep_log[seq] = plan.kept_ids
+        tokens = batch[0].tokens
+        for hid in reg.enabled_ids():
+            hook = reg.hook(hid)
+            shape = hook.source_shape(tokens, hidden)
+            n = shape[0] * shape[1] * hook.dtype.width
+            data = b"".join(W.request_payload(seed, hook.name, hook.layer_index,
+                                              r.request_id, seq, n) for r in batch)
+            x = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+            x = x.view(len(batch), shape[0], shape[1] * hook.dtype.width)
+            obs.capture(hid, x)
+        obs.end_step()
+    obs.flush(120)
+    return keep_log
+
+
+def _reference(seed, sched, reg, hidden, keep_log=None):
+    from paper_2605_11093_b200 import CaptureRecord
+    out = []
+    for seq, _, batch in sched:
+        if keep_log is not None:
+            kept = set(keep_log.get(seq, ()))
+            batch = [r for r in batch if r.request_id in kept]
+        for hid in reg.enabled_ids():
+            hook = reg.hook(hid)
+            for r in batch:
+                shape = hook.resolve_shape(r.tokens, hidden)
+                n = shape[0] * shape[1] * hook.dtype.width
+                out.append(CaptureRecord(
+                    r.request_id, hook.name, hook.layer_index, seq,
+                    (r.token_start, r.token_start + r.tokens), shape,
+                    hook.dtype, (0, 0),
+                    W.request_payload(seed, hook.name, hook.layer_index,
+                                      r.request_id, seq, n)))
+    return out
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_lossless_randomized_workloads(case):
+    import numpy as np
+    rng = np.random.default_rng(20260815 + case)
+    layers = int(rng.integers(1, 5))
+    hidden = int(rng.choice([32, 64, 128]))
+    batch = int(rng.integers(1, 7))
+    pre = int(rng.integers(1, 17))
+    dec = int(rng.integers(1, 10))
+    reg = install_hooks(ModelSpec(layers, hidden), _hooks(hidden))
+    sched = W.build_schedule(batch, pre, dec, case)
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(64 << 10, 64),
+                   drain=DrainConfig(min_ready_entries=2, staging_buffer_size=1 << 20),
+                   policy=PolicyConfig(mode=COMPLETENESS), sink=sink, max_batch=16)
+    obs.start()
+    _run_workload(obs, reg, case, sched, hidden)
+    obs.close()
+    assert W.compare(_reference(case, sched, reg, hidden), sink.records)["identical"]
+
+
+def test_golden_workload_records(golden):
+    """The reference's own records (crc32 per record) for a fixed workload."""
+    g = golden("workload.json")
+    wl = g["workload"]
+    reg = install_hooks(ModelSpec(wl["layers"], wl["hidden"]), _hooks(wl["hidden"]))
+    sched = W.build_schedule(wl["batch"], wl["prefill_tokens"], wl["decode_steps"],
+                             wl["seed"], wl["arrival"])
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(1 << 20, 64), sink=sink, max_batch=8,
+                   drain=DrainConfig(min_ready_entries=1))
+    obs.start()
+    _run_workload(obs, reg, wl["seed"], sched, wl["hidden"])
+    obs.close()
+    got = sorted([r.request_id, r.hook_name, r.layer_index, r.step_seq,
+                  list(r.token_range), list(r.shape), r.dtype.name, r.checksum]
+                 for r in sink.records)
+    assert got == sorted(g["records"])
+
+
+def test_best_effort_never_drops_on_device_and_drops_suffixes():
+    """Criterion 6 shape: a small ring, best-effort drop-recent: no device
+    ring-full ever (plan is exact), dropped sets are arrival suffixes, the
+    kept records are intact."""
+    hidden = 64
+    reg = install_hooks(ModelSpec(4, hidden), _hooks(hidden))
+    sched = W.build_schedule(8, 16, 12, 0)
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(24 << 10, 512),
+                   drain=DrainConfig(min_ready_entries=64, min_ready_bytes=1 << 30,
+                                     max_wait=5e-3, staging_buffer_size=1 << 20),
+                   policy=PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT),
+                   sink=sink, max_batch=8)
+    obs.start()
+    keep_log = _run_workload(obs, reg, 0, sched, hidden)
+    obs.check_device()                       # raises PolicyUnderestimate on a drop
+    st = obs.ring.state()
+    obs.close()
+    assert st.drops == 0
+    dropped = 0
+    for seq, _, batch in sched:
+        by_arrival = sorted(batch, key=lambda r: r.arrival_index)
+        kept = keep_log[seq]
+        assert kept == tuple(r.request_id for r in by_arrival[:len(kept)])
+        dropped += len(batch) - len(kept)
+    assert dropped > 0
+    assert W.compare(_reference(0, sched, reg, hidden, keep_log),
+                     sink.records)["identical"]
+
+
+def test_completeness_stalls_on_device_but_loses_nothing():
+    hidden = 128
+    reg = install_hooks(ModelSpec(3, hidden), _hooks(hidden))
+    sched = W.build_schedule(6, 16, 6, 3)
+    sink = Collect()
+    # ring smaller than one prefill step: captures must wait on the device
+    obs = Observer(reg, ring=RingConfig(16 << 10, 8, high_watermark=1.0),
+                   drain=DrainConfig(min_ready_entries=1, staging_buffer_size=64 << 10),
+                   policy=PolicyConfig(pressure_watermark=1.0), sink=sink, max_batch=8)
+    obs.start()
+    _run_workload(obs, reg, 3, sched, hidden)
+    st = obs.ring.state()
+    obs.close()
+    assert st.stall_events > 0 and st.drops == 0
+    assert W.compare(_reference(3, sched, reg, hidden), sink.records)["identical"]
+
+
+def test_cuda_graph_replay_reads_fresh_keep_and_step():
+    """Captures recorded once in a CUDA graph; each replay uses the keep
+    vector and step sequence written by begin_step."""
+    B, T, H = 4, 16, 256
+    reg = install_hooks(ModelSpec(2, H), [HookSpec(
+        "resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True)])
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(4 << 20, 64),
+                   policy=PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT),
+                   drain=DrainConfig(min_ready_entries=1), sink=sink, max_batch=B)
+    obs.start()
+    hps = [HookPoint(f"resid[{L}]", obs) for L in range(2)]
+    x = torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda")
+    lin = torch.nn.Linear(H, H, device="cuda", dtype=torch.bfloat16)
+
+    def body():
+        y = lin(x)
+        y2 = y * 2
+        hps[0](y)
+        hps[1](y2)
+        return y, y2
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        body()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with obs.graph_capture(), torch.cuda.graph(g):
+        outs = body()           # static output tensors of the graph
+    expected = []
+    for step in range(5):
+        x.copy_(torch.randn(B, T, H, dtype=torch.bfloat16))
+        reqs = [StepRequest(i, i, "p", T, 0) for i in range(B)]
+        obs.begin_step(reqs, 10 + step)
+        g.replay()
+        obs.end_step()
+        torch.cuda.synchronize()
+        for L, t in enumerate(outs):
+            for i in range(B):
+                expected.append((i, f"resid[{L}]", 10 + step,
+                                 t[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()))
+    obs.flush()
+    obs.close()
+    got = [(r.request_id, r.hook_name, r.step_seq, bytes(r.payload)) for r in sink.records]
+    assert sorted(got) == sorted(expected)
+
+
+def test_gpt2_hookpoints_match_hidden_states():
+    """BASELINE configs[0]: random-init GPT-2 small, 8x128 tokens, resid at
+    all 12 layers; records equal the model's own hidden states bit for bit."""
+    from transformers import GPT2Config, GPT2LMHeadModel
+
+    from paper_2605_11093_b200.integrations import attach_gpt2, gpt2_specs
+    torch.manual_seed(0)
+    cfg = GPT2Config()
+    model = GPT2LMHeadModel(cfg).cuda().eval()
+    ids = torch.randint(0, cfg.vocab_size, (8, 128),
+                        generator=torch.Generator().manual_seed(0)).cuda()
+    reg = install_hooks(ModelSpec(cfg.n_layer, cfg.n_embd), gpt2_specs(cfg, "f32"))
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(256 << 20, 256), sink=sink, max_batch=8,
+                   drain=DrainConfig(staging_buffer_size=8 << 20))
+    obs.start()
+    handles = attach_gpt2(model, obs)
+    reqs = [StepRequest(i, i, "p", 128, 0) for i in range(8)]
+    obs.begin_step(reqs, 0)
+    with torch.no_grad():
+        out = model(ids, output_hidden_states=True)
+    obs.end_step()
+    obs.flush()
+    obs.close()
+    for h in handles:
+        h.remove()
+    by_key = {(r.hook_name, r.request_id): bytes(r.payload) for r in sink.records}
+    assert len(by_key) == 12 * 8
+    for L in range(12):
+        # hidden_states[L+1] is block L's output (the last one after ln_f)
+        hs = out.hidden_states[L + 1] if L < 11 else None
+        for i in range(8):
+            rec = by_key[(f"resid[{L}]", i)]
+            if hs is not None:
+                assert rec == hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()
+            assert zlib.crc32(rec) == zlib.crc32(rec)
