@@ -920,6 +920,175 @@ __global__ void __launch_bounds__(kTmaThreads, 1) capture_tma_kernel(CapParams P
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory staged capture (COPY, 16-B aligned rows): every thread
+// issues cp.async (LDGSTS) 16-B copies of the CTA's slice into a double
+// buffer of 2 x 32 KiB, so up to 192 KiB per SM are in flight with few
+// registers; the first chunk is requested before the reservation is
+// known. Stores go smem -> ring with 128-bit STG, coalesced.
+// ---------------------------------------------------------------------------
+constexpr int kStgThreads = 256;
+constexpr int kStgWarps = kStgThreads / 32;
+constexpr int kStgChunk = 32 * 1024;
+constexpr int kStgCtasPerSm = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kStgThreads, kStgCtasPerSm) capture_stage_kernel(CapParams P) {
+  extern __shared__ __align__(128) uint8_t sbuf[];  // 2 x kStgChunk
+  __shared__ CapShared sh;
+  const int tid = threadIdx.x;
+  const int64_t U = P.units;
+  const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
+
+  // ---- 1. ordered compaction ----
+  int64_t u0 = 0, u1 = 0;
+  uint32_t mycnt = 0, mybase = 0;
+  uint64_t K;
+  if (P.keep) {
+    int64_t per = (U + kStgThreads - 1) / kStgThreads;
+    if (P.keep_vec) per = (per + 15) & ~int64_t(15);
+    u0 = imin64(int64_t(tid) * per, U);
+    u1 = imin64(u0 + per, U);
+    int64_t u = u0;
+    if (P.keep_vec) {
+      for (; u + 16 <= u1; u += 16) {
+        uint4 k = *reinterpret_cast<const uint4*>(P.keep + u);
+        mycnt += count_nonzero_bytes(k.x) + count_nonzero_bytes(k.y) +
+                 count_nonzero_bytes(k.z) + count_nonzero_bytes(k.w);
+      }
+    }
+    for (; u < u1; ++u) mycnt += P.keep[u] != 0;
+    mybase = block_exclusive_scan<kStgWarps>(mycnt, sh);
+    K = sh.total;
+  } else {
+    K = (uint64_t)U;
+  }
+  const uint64_t n_rows = K * (uint64_t)P.rpu;
+  if (n_rows == 0) {
+    if (blockIdx.x == 0 && tid == 0) {
+      tf_capture_result& r = P.ctl->res;
+      r.capture_seq = 0;
+      r.status = TF_OK;
+      r.n_rows = 0;
+      r.payload_len = 0;
+      r.ready_seq = TF_READY_SENTINEL;
+    }
+    return;
+  }
+  const uint32_t row_w = uint32_t(P.out_row_bytes / 16);  // 16-B words per row
+  const uint64_t total_w = n_rows * row_w;
+
+  // ---- 2. this CTA's word range and rank table ----
+  const uint64_t per_cta = (total_w + gridDim.x - 1) / gridDim.x;
+  const uint64_t w0 = min(total_w, uint64_t(blockIdx.x) * per_cta);
+  const uint64_t w1 = min(total_w, w0 + per_cta);
+  const int64_t r_lo = int64_t(w0 / row_w) / P.rpu;
+  if (P.keep && w0 < w1) {
+    const int64_t r_hi = int64_t((w1 - 1) / row_w) / P.rpu;
+    if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
+      int64_t rank = mybase;
+      for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
+        if (P.keep[u]) {
+          if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
+          ++rank;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  auto src_word = [&](uint64_t w) -> const uint8_t* {
+    const uint64_t j = w / row_w;
+    const uint64_t k = w - j * row_w;
+    const int64_t r = int64_t(j) / P.rpu;
+    const int64_t sub = int64_t(j) - r * P.rpu;
+    const int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
+    return row_src(P, unit * P.rpu + sub) + k * 16;
+  };
+  constexpr uint32_t kChunkW = kStgChunk / 16;
+  const uint32_t nchunks = uint32_t((w1 - w0 + kChunkW - 1) / kChunkW);
+  auto load_chunk = [&](uint32_t c) {
+    const uint64_t cw0 = w0 + uint64_t(c) * kChunkW;
+    const uint64_t cw1 = min(w1, cw0 + kChunkW);
+    uint8_t* buf = sbuf + (c & 1) * kStgChunk;
+    for (uint64_t w = cw0 + tid; w < cw1; w += kStgThreads)
+      cp_async16(buf + (w - cw0) * 16, src_word(w));
+    cp_async_commit();
+  };
+
+  // ---- 3. prefetch chunk 0, then learn the offset ----
+  if (nchunks > 0) load_chunk(0);
+  if (tid == 0) {
+    uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
+    if (t == 0) {
+      P.ctl->k_t0 = t_entry;
+      leader_reserve(P, total_w * 16, n_rows);
+      __threadfence();
+      st_release_gpu(&P.ctl->plan_flag, 1u);
+    } else {
+      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+    }
+    sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
+    sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+  }
+  __syncthreads();
+  const bool ok = sh.status == TF_OK;
+  uint8_t* dst_base = P.payload + sh.off;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    if (ok && c + 1 < nchunks) {
+      load_chunk(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // chunk c landed for every thread
+    if (ok) {
+      const uint64_t cw0 = w0 + uint64_t(c) * kChunkW;
+      const uint64_t cw1 = min(w1, cw0 + kChunkW);
+      const uint8_t* buf = sbuf + (c & 1) * kStgChunk;
+#pragma unroll 4
+      for (uint64_t w = cw0 + tid; w < cw1; w += kStgThreads) {
+        uint4 v = *reinterpret_cast<const uint4*>(buf + (w - cw0) * 16);
+        *reinterpret_cast<uint4*>(dst_base + w * 16) = v;
+      }
+    } else {
+      break;  // rejected: chunk 0 drained above, nothing else was issued
+    }
+    __syncthreads();  // buffer (c & 1) is free for chunk c + 2
+  }
+
+  // ---- 4. the last CTA to retire publishes ----
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    uint32_t t = atomicAdd(&P.ctl->done, 1u);
+    sh.is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (sh.is_last) {
+    if (tid == 0) {
+      __threadfence();
+      last_cta_prepare(P, sh);
+    }
+    __syncthreads();
+    if (sh.publish && tid < 8) sh.slot[tid] = sh.desc[tid];
+    if (tid == 0) {
+      P.ctl->arrive = 0;
+      P.ctl->done = 0;
+      P.ctl->plan_flag = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Protocol-level producer ops (single thread): the same allocator and
 // publish rules exposed one call at a time, for the reference's ring tests.
 __global__ void reserve_kernel(CapParams P, uint64_t len) {
@@ -1229,10 +1398,31 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (a->op == TF_OP_COPY) {
     int vw = std::min<int>(sal, pow2_align((uint64_t)a->row_bytes));
     P.words_per_row = a->row_bytes / vw;
-    static int copy_path = -1;  // 0 = LDG/STG warps, 1 = TMA bulk copies
+    // 0 = LDG/STG warps (default: measured fastest on B200),
+    // 1 = TMA bulk copies, 2 = cp.async smem staging (TF_COPY_PATH=tma|stage)
+    static int copy_path = -1;
     if (copy_path < 0) {
       const char* e = getenv("TF_COPY_PATH");
-      copy_path = (e && e[0] == 'l') ? 0 : 1;
+      copy_path = (e && e[0] == 't') ? 1 : (e && e[0] == 's') ? 2 : 0;
+    }
+    if (vw == 16 && copy_path == 2) {
+      static bool attr2 = false;
+      if (!attr2) {
+        CUDA_TRY(cudaFuncSetAttribute(capture_stage_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStgChunk));
+        attr2 = true;
+      }
+      int g = int(std::min<uint64_t>((out_max + (16u << 10) - 1) / (16u << 10),
+                                     uint64_t(g_sm_count) * kStgCtasPerSm));
+      g = std::max(std::max(g, grid_table), 1);
+      if (a->max_ctas) g = std::max(grid_table, std::min<int>(g, (int)a->max_ctas));
+      capture_stage_kernel<<<g, kStgThreads, 2 * kStgChunk, s>>>(P);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        tf_set_error("capture launch: %s", cudaGetErrorString(e));
+        return TF_ERR_CUDA;
+      }
+      return TF_OK;
     }
     if (vw == 16 && copy_path == 1) {
       static bool attr_set = false;

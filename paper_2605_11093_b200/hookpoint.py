@@ -198,6 +198,9 @@ class Observer:
         if st.device_errors & N.TF_DEVERR_TIMEOUT:
             from .errors import DeviceError
             raise DeviceError("device wait for ring space timed out")
+        if st.device_errors & N.TF_DEVERR_TOO_LARGE:
+            raise ValueError("a capture exceeded the payload ring capacity "
+                             "(rings.py:297-298)")
 
     def _sampled_names(self) -> set:
         return {self.registry.hook(h).name for h in self.sampled_hooks}

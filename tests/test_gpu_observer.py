@@ -150,10 +150,19 @@ def test_completeness_stalls_on_device_but_loses_nothing():
     hidden = 128
     reg = install_hooks(ModelSpec(3, hidden), _hooks(hidden))
     sched = W.build_schedule(6, 16, 6, 3)
-    sink = Collect()
-    # ring smaller than one prefill step: captures must wait on the device
-    obs = Observer(reg, ring=RingConfig(16 << 10, 8, high_watermark=1.0),
-                   drain=DrainConfig(min_ready_entries=1, staging_buffer_size=64 << 10),
+    class SlowSink(Collect):
+        def write(self, recs):
+            import time
+            time.sleep(0.02)
+            super().write(recs)
+
+    sink = SlowSink()
+    # ring smaller than one prefill step (largest capture 24 KiB, step
+    # 75 KiB) and a slow sink behind a one-buffer pipeline: captures must
+    # wait on the device for the consumer
+    obs = Observer(reg, ring=RingConfig(32 << 10, 8, high_watermark=1.0),
+                   drain=DrainConfig(min_ready_entries=1, staging_buffer_size=64 << 10,
+                                     staging_buffer_count=1, stage_queue_slots=1),
                    policy=PolicyConfig(pressure_watermark=1.0), sink=sink, max_batch=8)
     obs.start()
     _run_workload(obs, reg, 3, sched, hidden)
