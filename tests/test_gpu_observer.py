@@ -252,7 +252,7 @@ def test_gpt2_hookpoints_match_hidden_states():
         # hidden_states[L+1] is block L's output (the last one after ln_f)
         hs = out.hidden_states[L + 1] if L < 11 else None
         for i in range(8):
-            rec = by_key[(f"resid[{L}]", i)]
+            rec = by_key[(f"resid_post[{L}]", i)]
             if hs is not None:
                 assert rec == hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()
             assert zlib.crc32(rec) == zlib.crc32(rec)
