@@ -703,8 +703,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     if (tid == 0) {  // re-arm the handshake for the next launch on this stream
       P.ctl->arrive = 0;
       P.ctl->done = 0;
-      P.ctl->plan_flag = 0;
-      __threadfence();
+      P.ctl->plan_flag = 0;  // visible to the next launch (kernel boundary)
     }
   }
 }
@@ -914,8 +913,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) capture_tma_kernel(CapParams P
     if (tid == 0) {
       P.ctl->arrive = 0;
       P.ctl->done = 0;
-      P.ctl->plan_flag = 0;
-      __threadfence();
+      P.ctl->plan_flag = 0;  // visible to the next launch (kernel boundary)
     }
   }
 }
@@ -1083,8 +1081,7 @@ __global__ void __launch_bounds__(kStgThreads, kStgCtasPerSm) capture_stage_kern
     if (tid == 0) {
       P.ctl->arrive = 0;
       P.ctl->done = 0;
-      P.ctl->plan_flag = 0;
-      __threadfence();
+      P.ctl->plan_flag = 0;  // visible to the next launch (kernel boundary)
     }
   }
 }

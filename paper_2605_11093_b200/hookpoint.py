@@ -91,8 +91,16 @@ class Observer:
         self.rank_coords = rank_coords
         dev = f"cuda:{self.device}"
         self.keep_req = t.ones(max_batch, dtype=t.uint8, device=dev)
-        self.keep_tok = t.zeros(max(1, max_rows_sampled), dtype=t.uint8,
-                                device=dev)
+        # per-token keep for sampled hooks, expanded over each hook's row
+        # groups: a (heads, tokens, tokens) attention map has `heads` query
+        # rows per token; fixed buffers so CUDA-graph replays see updates
+        self._groups = {h: _row_groups(registry.hook(h), registry.hidden_extent)
+                        for h in self.sampled_hooks}
+        self._keep_m = {}
+        for m in sorted(set(self._groups.values())):
+            n = min(max_rows_sampled, max_batch * m * max_tokens)
+            self._keep_m[m] = t.zeros(max(1, n), dtype=t.uint8, device=dev)
+        self.keep_tok = self._keep_m.get(1)
         self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
         self.max_batch = max_batch
         self._names = {h.name: i for i, h in enumerate(registry.hooks)}
@@ -143,8 +151,10 @@ class Observer:
             for r in kept:
                 sel[r.request_id] = self.sampler.select(r.request_id, step_seq,
                                                         r.tokens)
-            metas = [self._sampled_meta(m, kept, sel)
-                     if m.hook_name in self._sampled_names() else m
+            groups = {self.registry.hook(h).name: g
+                      for h, g in self._groups.items()}
+            metas = [self._sampled_meta(m, kept, sel, groups[m.hook_name])
+                     if m.hook_name in groups else m
                      for m in metas]
         self.fifo.extend(metas)
         s = stream if stream is not None else t.cuda.current_stream(self.device)
@@ -155,12 +165,15 @@ class Observer:
             self.step_buf.copy_(step, non_blocking=True)
             if sel:
                 tokens = batch[0].tokens
-                flags = [0] * (len(batch) * tokens)
+                flags = t.zeros(len(batch), 1, tokens, dtype=t.uint8)
                 for i, r in enumerate(batch):
                     for tok in sel.get(r.request_id, ()):
-                        flags[i * tokens + tok] = 1
-                kt = t.tensor(flags, dtype=t.uint8).pin_memory()
-                self.keep_tok[:kt.numel()].copy_(kt, non_blocking=True)
+                        flags[i, 0, tok] = 1
+                for m, buf in self._keep_m.items():
+                    kt = flags.expand(len(batch), m, tokens).reshape(-1)
+                    if kt.numel() > buf.numel():
+                        raise ConfigError("sampled keep vector exceeds its buffer")
+                    buf[:kt.numel()].copy_(kt.pin_memory(), non_blocking=True)
         self._plan, self._batch, self._tok_sel = plan, batch, sel
         self.active = bool(plan.kept_ids)
         self.steps += 1
@@ -202,12 +215,11 @@ class Observer:
             raise ValueError("a capture exceeded the payload ring capacity "
                              "(rings.py:297-298)")
 
-    def _sampled_names(self) -> set:
-        return {self.registry.hook(h).name for h in self.sampled_hooks}
-
-    def _sampled_meta(self, meta: TensorMeta, kept, sel) -> TensorMeta:
-        counts = tuple(len(sel[r.request_id]) for r in kept)
-        per_row_shape = tuple(meta.shape[1:])
+    def _sampled_meta(self, meta: TensorMeta, kept, sel, groups: int) -> TensorMeta:
+        # rows of request i: `groups` x its kept tokens, in memory order
+        # (group-major, e.g. head-major for attention maps)
+        counts = tuple(groups * len(sel[r.request_id]) for r in kept)
+        per_row_shape = tuple(meta.shape[-1:])
         return TensorMeta(
             hook_name=meta.hook_name, layer_index=meta.layer_index,
             step_seq=meta.step_seq, request_ids=meta.request_ids,
@@ -228,14 +240,30 @@ class Observer:
             return
         hook = self.registry.hook(hook_id)
         src = _rows_of(x, hook)
-        sampled = hook_id in self.sampled_hooks and self._tok_sel
+        sampled = hook_id in self.sampled_hooks and bool(self._tok_sel)
+        keep = self._keep_m[self._groups[hook_id]] if sampled else self.keep_req
         args = capture_args(
-            src, hook_id=hook_id, hook=hook,
-            keep_ptr=(self.keep_tok if sampled else self.keep_req).data_ptr(),
+            src, hook_id=hook_id, hook=hook, keep_ptr=keep.data_ptr(),
             keep_per_outer=not sampled, step_seq_ptr=self.step_buf.data_ptr(),
             full=self.policy.full_mode)
         launch_capture(self.ring, args, stream)
         self.launches += 1
+
+
+def _row_groups(hook, hidden: int) -> int:
+    """Row groups per token of a sampled hook: rows per request divided by
+    the token count, e.g. `heads` for a (heads, tokens, tokens) map."""
+    lead = hook.dims[:-1]
+    if lead.count("tokens") != 1:
+        raise ConfigError(
+            f"sampled hook {hook.name!r} needs exactly one leading tokens axis")
+    m = 1
+    for d in lead:
+        if d == "hidden":
+            m *= hidden
+        elif not isinstance(d, str):
+            m *= d
+    return m
 
 
 def _rows_of(x, hook) -> RowSource:
@@ -288,4 +316,4 @@ def ceil_div(a: int, b: int) -> int:
 
 
 __all__ = ["HookPoint", "Observer", "TokenSampler", "total_step_bytes",
-           "ceil_div", "math"]
+           "ceil_div"]

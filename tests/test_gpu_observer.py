@@ -256,3 +256,68 @@ def test_gpt2_hookpoints_match_hidden_states():
             if hs is not None:
                 assert rec == hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()
             assert zlib.crc32(rec) == zlib.crc32(rec)
+
+
+def test_llama_attention_kv_token_sampling():
+    """BASELINE configs[2] in miniature: eager-attention Llama, attention
+    probabilities and KV projections captured, token-sampling policy on the
+    attention map and the residual stream (every 4th query token)."""
+    from paper_2605_11093_b200.hookpoint import TokenSampler
+    from paper_2605_11093_b200.integrations import (attach_llama, llama_registry,
+                                                    random_llama)
+    from transformers import LlamaConfig
+    cfg = LlamaConfig(hidden_size=256, intermediate_size=512, num_hidden_layers=2,
+                      num_attention_heads=4, num_key_value_heads=2,
+                      vocab_size=1000, max_position_embeddings=128)
+    cfg._attn_implementation = "eager"
+    model = random_llama(cfg)
+    sites = ("k_slice", "v_slice", "attn_pattern", "resid_post")
+    reg = llama_registry(cfg, sites)
+    sampled = frozenset(i for i, h in enumerate(reg.hooks)
+                        if h.name.startswith(("attn_pattern", "resid_post")))
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(16 << 20, 256), sink=sink, max_batch=4,
+                   max_tokens=64, sampler=TokenSampler(every=4),
+                   sampled_hooks=sampled, drain=DrainConfig(min_ready_entries=1))
+    obs.start()
+    ref = {}
+
+    def keep_ref(name):
+        def hook(m, a, out):
+            t = out[1] if name.startswith("attn") else (out[0] if isinstance(out, tuple) else out)
+            ref[name] = t.detach().clone()
+        return hook
+    inner = model.model
+    handles = []
+    for L, layer in enumerate(inner.layers):
+        handles.append(layer.self_attn.register_forward_hook(keep_ref(f"attn_pattern[{L}]")))
+        handles.append(layer.self_attn.k_proj.register_forward_hook(keep_ref(f"k_slice[{L}]")))
+        handles.append(layer.self_attn.v_proj.register_forward_hook(keep_ref(f"v_slice[{L}]")))
+        handles.append(layer.register_forward_hook(keep_ref(f"resid_post[{L}]")))
+    handles += attach_llama(model, obs, sites)
+    B, T = 3, 32
+    ids = torch.randint(0, 1000, (B, T), device="cuda")
+    obs.begin_step([StepRequest(10 + i, i, "p", T, 0) for i in range(B)], 5)
+    with torch.inference_mode():
+        model.model(input_ids=ids, use_cache=False)
+    obs.end_step()
+    obs.flush()
+    obs.close()
+    for h in handles:
+        h.remove()
+    got = {(r.hook_name, r.request_id): r for r in sink.records}
+    assert len(got) == 4 * 2 * B
+    kept_tok = list(range(0, T, 4))
+    for L in range(2):
+        for i in range(B):
+            a = got[(f"attn_pattern[{L}]", 10 + i)]
+            want = ref[f"attn_pattern[{L}]"][i][:, kept_tok, :].contiguous()
+            assert a.shape == (4 * len(kept_tok), T)
+            assert bytes(a.payload) == want.view(torch.uint8).cpu().numpy().tobytes()
+            r = got[(f"resid_post[{L}]", 10 + i)]
+            want = ref[f"resid_post[{L}]"][i][kept_tok].contiguous()
+            assert bytes(r.payload) == want.view(torch.uint8).cpu().numpy().tobytes()
+            for kv in ("k_slice", "v_slice"):
+                k = got[(f"{kv}[{L}]", 10 + i)]
+                want = ref[f"{kv}[{L}]"][i].contiguous()
+                assert bytes(k.payload) == want.view(torch.uint8).cpu().numpy().tobytes()
