@@ -402,6 +402,18 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
   }
 }
 
+// Non-leader CTAs wait for the leader's plan with exponential backoff: under
+// completeness the leader may wait milliseconds for ring space, and a tight
+// poll of one L2 line by hundreds of CTAs taxes the memory system the
+// staging copy engine is reading from.
+__device__ __forceinline__ void wait_plan(DevCtl* c) {
+  uint32_t ns = 32;
+  while (ld_acquire_gpu(&c->plan_flag) == 0) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? ns * 2 : ns;
+  }
+}
+
 // Last CTA, thread 0: build the descriptor and the result record; the
 // caller posts the descriptor with one coalesced warp store.
 __device__ void last_cta_prepare(const CapParams& P, CapShared& sh) {
@@ -560,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     }
     if (tid == 0) {
       if (!leader)
-        while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+        wait_plan(P.ctl);
       sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
       sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
     }
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   } else {
     if (tid == 0) {
       if (!leader)
-        while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+        wait_plan(P.ctl);
       sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
       sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
     }
@@ -867,7 +879,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) capture_tma_kernel(CapParams P
       __threadfence();
       st_release_gpu(&P.ctl->plan_flag, 1u);
     } else {
-      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+      wait_plan(P.ctl);
     }
     const uint32_t status = *((volatile uint32_t*)&P.ctl->plan_status);
     uint8_t* dst_base = P.payload + *((volatile uint64_t*)&P.ctl->plan_off);
@@ -1032,7 +1044,7 @@ __global__ void __launch_bounds__(kStgThreads, kStgCtasPerSm) capture_stage_kern
       __threadfence();
       st_release_gpu(&P.ctl->plan_flag, 1u);
     } else {
-      while (ld_acquire_gpu(&P.ctl->plan_flag) == 0) __nanosleep(20);
+      wait_plan(P.ctl);
     }
     sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
     sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
