@@ -270,7 +270,8 @@ def leg_value(args, dist, dev):
             run_step(3)
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g0.record(prod)
-    graph.replay()
+    with torch.cuda.stream(prod):
+        graph.replay()      # replays on the current stream
     g1.record(prod)
     prod.synchronize()
     ring.note_launch(prod)
