@@ -101,7 +101,12 @@ class Observer:
             n = min(max_rows_sampled, max_batch * m * max_tokens)
             self._keep_m[m] = t.zeros(max(1, n), dtype=t.uint8, device=dev)
         self.keep_tok = self._keep_m.get(1)
+        self._flat = {}
+        self._flat_rows = max_batch * 64
+        self._layout = "batch"
         self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
+        self.token = t.zeros(1, dtype=t.uint8, device=dev)  # custom-op ordering token
+        self.index = _register_observer(self)
         self.max_batch = max_batch
         self._names = {h.name: i for i, h in enumerate(registry.hooks)}
         self._plan: StepPlan | None = None
@@ -133,21 +138,33 @@ class Observer:
 
     # -- per step --------------------------------------------------------------
 
-    def begin_step(self, batch, step_seq: int, stream=None) -> StepPlan:
-        """Plan the step, honour the flush gate, queue metadata, upload keep."""
+    def begin_step(self, batch, step_seq: int, stream=None,
+                   layout: str = "batch") -> StepPlan:
+        """Plan the step, honour the flush gate, queue metadata, upload keep.
+
+        ``layout="batch"``: activations are (B, T, ...) with uniform T
+        (the reference's model). ``layout="flat"``: continuous batching —
+        activations are (sum of tokens, ...) in batch order and requests may
+        carry different token counts (prefill chunks beside decodes).
+        """
         t = torch()
         batch = list(batch)
         if len(batch) > self.max_batch:
             raise ConfigError("batch exceeds the observer's max_batch")
+        if layout not in ("batch", "flat"):
+            raise ConfigError(f"unknown activation layout {layout!r}")
+        flat = layout == "flat"
         self.registry.commit_filter()
         plan = prepare_step(self.policy, batch, self.ring, self.registry,
-                            step_seq=step_seq, rank_coords=self.rank_coords)
+                            step_seq=step_seq, rank_coords=self.rank_coords,
+                            ragged=flat)
         if plan.flush_before:
             self.flush()
         metas = list(plan.fifo_entries)
         sel = {}
+        kept_set = set(plan.kept_ids)
         if self.sampler is not None and plan.kept_ids and self.sampled_hooks:
-            kept = [r for r in batch if r.request_id in set(plan.kept_ids)]
+            kept = [r for r in batch if r.request_id in kept_set]
             for r in kept:
                 sel[r.request_id] = self.sampler.select(r.request_id, step_seq,
                                                         r.tokens)
@@ -159,25 +176,56 @@ class Observer:
         self.fifo.extend(metas)
         s = stream if stream is not None else t.cuda.current_stream(self.device)
         with t.cuda.stream(s):
-            keep = t.tensor(list(plan.keep) or [0], dtype=t.uint8).pin_memory()
-            self.keep_req[:keep.numel()].copy_(keep, non_blocking=True)
             step = t.tensor([step_seq & 0x7FFFFFFF], dtype=t.int32).pin_memory()
             self.step_buf.copy_(step, non_blocking=True)
-            if sel:
-                tokens = batch[0].tokens
-                flags = t.zeros(len(batch), 1, tokens, dtype=t.uint8)
-                for i, r in enumerate(batch):
-                    for tok in sel.get(r.request_id, ()):
-                        flags[i, 0, tok] = 1
-                for m, buf in self._keep_m.items():
-                    kt = flags.expand(len(batch), m, tokens).reshape(-1)
-                    if kt.numel() > buf.numel():
-                        raise ConfigError("sampled keep vector exceeds its buffer")
-                    buf[:kt.numel()].copy_(kt.pin_memory(), non_blocking=True)
+            if flat:
+                # per-row keep over the flat token layout
+                rows = sum(r.tokens for r in batch)
+                flags = t.zeros(max(1, rows), dtype=t.uint8)
+                samp = t.zeros(max(1, rows), dtype=t.uint8)
+                pos = 0
+                for r in batch:
+                    if r.request_id in kept_set:
+                        flags[pos:pos + r.tokens] = 1
+                        for tok in sel.get(r.request_id, ()):
+                            samp[pos + tok] = 1
+                    pos += r.tokens
+                self._upload(self._flat_buf("req", rows), flags)
+                if sel:
+                    self._upload(self._flat_buf("tok", rows), samp)
+            else:
+                keep = t.tensor(list(plan.keep) or [0], dtype=t.uint8)
+                self._upload(self.keep_req, keep)
+                if sel:
+                    tokens = batch[0].tokens
+                    flags = t.zeros(len(batch), 1, tokens, dtype=t.uint8)
+                    for i, r in enumerate(batch):
+                        for tok in sel.get(r.request_id, ()):
+                            flags[i, 0, tok] = 1
+                    for m, buf in self._keep_m.items():
+                        self._upload(buf, flags.expand(len(batch), m, tokens).reshape(-1))
         self._plan, self._batch, self._tok_sel = plan, batch, sel
+        self._layout = layout
         self.active = bool(plan.kept_ids)
         self.steps += 1
         return plan
+
+    @staticmethod
+    def _upload(dst, src) -> None:
+        if src.numel() > dst.numel():
+            raise ConfigError("keep vector exceeds its device buffer")
+        dst[:src.numel()].copy_(src.pin_memory(), non_blocking=True)
+
+    def _flat_buf(self, kind: str, rows: int):
+        """Fixed per-row keep buffers for the flat layout (grown, never
+        moved while a CUDA graph may reference them)."""
+        t = torch()
+        buf = self._flat.get(kind)
+        if buf is None or buf.numel() < rows:
+            n = max(rows, self._flat_rows)
+            buf = t.zeros(n, dtype=t.uint8, device=f"cuda:{self.device}")
+            self._flat[kind] = buf
+        return buf
 
     def end_step(self, stream=None) -> None:
         self.ring.note_launch(stream)
@@ -239,12 +287,19 @@ class Observer:
         if not self.active or not self.registry.is_enabled(hook_id):
             return
         hook = self.registry.hook(hook_id)
-        src = _rows_of(x, hook)
         sampled = hook_id in self.sampled_hooks and bool(self._tok_sel)
-        keep = self._keep_m[self._groups[hook_id]] if sampled else self.keep_req
+        if self._layout == "flat":
+            # (sum of tokens, ...): one row per token, per-row keep
+            src = _token_rows(x)
+            keep = self._flat["tok" if sampled else "req"]
+            per_outer = False
+        else:
+            src = _rows_of(x, hook)
+            keep = self._keep_m[self._groups[hook_id]] if sampled else self.keep_req
+            per_outer = not sampled
         args = capture_args(
             src, hook_id=hook_id, hook=hook, keep_ptr=keep.data_ptr(),
-            keep_per_outer=not sampled, step_seq_ptr=self.step_buf.data_ptr(),
+            keep_per_outer=per_outer, step_seq_ptr=self.step_buf.data_ptr(),
             full=self.policy.full_mode)
         launch_capture(self.ring, args, stream)
         self.launches += 1
@@ -264,6 +319,19 @@ def _row_groups(hook, hidden: int) -> int:
         elif not isinstance(d, str):
             m *= d
     return m
+
+
+def _token_rows(x) -> RowSource:
+    """A flat (tokens, ...) activation as one row per token."""
+    if x.dim() < 1:
+        raise ConfigError("flat activations need a token axis")
+    x2 = x.reshape(x.shape[0], -1)
+    if x2.stride(-1) != 1:
+        x2 = x2.contiguous()
+    esz = x2.element_size()
+    row = x2.shape[1] * esz
+    return RowSource(x2.data_ptr(), x2.shape[0], 1, row, x2.stride(0) * esz,
+                     row, x2)
 
 
 def _rows_of(x, hook) -> RowSource:
@@ -301,9 +369,43 @@ class HookPoint(nn.Module):
 
     def forward(self, x):
         obs = self.observer
-        if obs is not None and self._hid is not None and obs.active:
+        if obs is None or self._hid is None:
+            return x
+        t = torch()
+        if t.compiler.is_compiling():
+            # traced as an opaque custom op (§3.1): the compiled
+            # graph keeps the capture launch and checks obs.active at run time
+            t.ops.ring2.capture(x, obs.token, obs.index, self._hid)
+        elif obs.active:
             obs.capture(self._hid, x)
         return x
+
+
+# ---------------------------------------------------------------------------
+# the custom operator behind HookPoint under torch.compile
+# ---------------------------------------------------------------------------
+_OBSERVERS: list = []
+
+
+def _register_observer(obs: Observer) -> int:
+    import weakref
+    _OBSERVERS.append(weakref.ref(obs))
+    return len(_OBSERVERS) - 1
+
+
+@torch().library.custom_op(
+    "ring2::capture", mutates_args=("token",),
+    schema="(Tensor x, Tensor(a!) token, int observer, int hook_id) -> ()")
+def _capture_op(x, token, observer, hook_id):
+    ref = _OBSERVERS[observer] if 0 <= observer < len(_OBSERVERS) else None
+    obs = ref() if ref is not None else None
+    if obs is not None and obs.active:
+        obs.capture(hook_id, x)
+
+
+@_capture_op.register_fake
+def _capture_fake(x, token, observer, hook_id) -> None:
+    return None
 
 
 def total_step_bytes(registry: HookRegistry, batch) -> int:

@@ -116,6 +116,85 @@ def test_golden_workload_records(golden):
     assert got == sorted(g["records"])
 
 
+@pytest.mark.parametrize("policy", ["completeness", "best-effort"])
+def test_flat_continuous_batching_layout(policy):
+    """Serving layout (vLLM-style): one (sum tokens, H) activation per hook
+    for a step mixing a prefill chunk and decodes; records are each
+    request's own token rows."""
+    H = 512
+    reg = install_hooks(ModelSpec(2, H), [HookSpec(
+        "resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True)])
+    pol = PolicyConfig() if policy == "completeness" else \
+        PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT)
+    ring_bytes = 1 << 20 if policy == "completeness" else 2 * 9 * H * 2 + 2 * 16
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(ring_bytes, 64), policy=pol, sink=sink,
+                   max_batch=8, drain=DrainConfig(min_ready_entries=1))
+    obs.start()
+    steps = [[StepRequest(1, 0, "a", 7, 0), StepRequest(2, 1, "b", 1, 30),
+              StepRequest(3, 2, "c", 3, 11)],
+             [StepRequest(1, 0, "a", 1, 7), StepRequest(2, 1, "b", 1, 31),
+              StepRequest(3, 2, "c", 1, 14), StepRequest(4, 3, "d", 5, 0)]]
+    expected = []
+    for seq, batch in enumerate(steps):
+        rows = sum(r.tokens for r in batch)
+        xs = [torch.randn(rows, H, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+        plan = obs.begin_step(batch, seq, layout="flat")
+        for L in range(2):
+            obs.capture(reg.id_of(f"resid[{L}]"), xs[L])
+        obs.end_step()
+        pos = 0
+        for r in batch:
+            if r.request_id in plan.kept_ids:
+                for L in range(2):
+                    expected.append((r.request_id, f"resid[{L}]", seq,
+                                     (r.token_start, r.token_start + r.tokens),
+                                     (r.tokens, H),
+                                     xs[L][pos:pos + r.tokens].contiguous()
+                                     .view(torch.uint8).cpu().numpy().tobytes()))
+            pos += r.tokens
+        obs.flush()
+    obs.check_device()
+    obs.close()
+    got = [(r.request_id, r.hook_name, r.step_seq, tuple(r.token_range),
+            tuple(r.shape), bytes(r.payload)) for r in sink.records]
+    assert sorted(got) == sorted(expected)
+    if policy == "best-effort":
+        assert len(expected) < 2 * 7     # something was dropped
+
+
+def test_hookpoint_under_torch_compile():
+    """The compiled graph keeps the capture (custom op) and reads the
+    observer's activity at run time."""
+    H = 256
+    reg = install_hooks(ModelSpec(1, H), [HookSpec(
+        "resid", ("tokens", "hidden"), DType.of("f32"), per_layer=True)])
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(1 << 20, 16), sink=sink, max_batch=4,
+                   drain=DrainConfig(min_ready_entries=1))
+    obs.start()
+    hp = HookPoint("resid[0]", obs)
+
+    def f(x):
+        y = torch.sin(x) * 2
+        hp(y)
+        return y + 1
+
+    cf = torch.compile(f, fullgraph=True)
+    x = torch.randn(2, 8, H, device="cuda")
+    cf(x)                                   # inactive: no capture
+    obs.begin_step([StepRequest(i, i, "p", 8, 0) for i in range(2)], 1)
+    out = cf(x)
+    obs.end_step()
+    obs.flush()
+    obs.close()
+    want = ((out - 1).view(2, -1))
+    assert len(sink.records) == 2
+    for r in sink.records:
+        got = torch.frombuffer(bytearray(bytes(r.payload)), dtype=torch.float32)
+        assert torch.equal(got, want[r.request_id].cpu())
+
+
 def test_best_effort_never_drops_on_device_and_drops_suffixes():
     """Criterion 6 shape: a small ring, best-effort drop-recent: no device
     ring-full ever (plan is exact), dropped sets are arrival suffixes, the

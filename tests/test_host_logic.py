@@ -232,6 +232,51 @@ def test_descriptor_wire_round_trip():
     assert d.reserved_len == 48 and Descriptor(0, 17, 0, 0).reserved_len == 32
 
 
+def test_hookpoint_custom_op_survives_tracing():
+    """PAPER.md §3.1: HookPoint dispatches a custom operator, so compiler
+    tracing keeps the capture as an opaque node instead of a Python hook."""
+    import torch
+    from torch.fx.experimental.proxy_tensor import make_fx
+
+    from paper_2605_11093_b200.hookpoint import _capture_op  # noqa: F401
+
+    def f(x, tok):
+        torch.ops.ring2.capture(x, tok, 0, 3)
+        return x + 1
+
+    g = make_fx(f, tracing_mode="fake")(torch.randn(2, 4),
+                                        torch.zeros(1, dtype=torch.uint8))
+    assert "ring2.capture.default" in [str(n.target) for n in g.graph.nodes]
+
+
+def test_ragged_continuous_batching_plan():
+    """Extension: mixed prefill chunk + decodes in one step."""
+    reg = install_hooks(ModelSpec(2, 16), [
+        HookSpec("resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+        HookSpec("logits", ("tokens", 8), DType.of("f32"))])
+    ring = OracleBackedRing(1 << 20, 64)
+    batch = [StepRequest(1, 0, "a", 5, 0), StepRequest(2, 1, "b", 1, 40),
+             StepRequest(3, 2, "c", 3, 7)]
+    with pytest.raises(ConfigError):
+        prepare_step(PolicyConfig(), batch, ring, reg, step_seq=0)
+    plan = prepare_step(PolicyConfig(), batch, ring, reg, step_seq=0, ragged=True)
+    assert [m.hook_name for m in plan.fifo_entries] == ["resid[0]", "resid[1]", "logits"]
+    m = plan.fifo_entries[0]
+    assert m.row_counts == (5, 1, 3) and m.shape == (5, 16)
+    assert m.token_ranges == ((0, 5), (40, 41), (7, 10))
+    assert m.expected_payload_len == 9 * 16 * 2
+    recs = split_payload(m, bytes(range(256)) + bytes(32))
+    assert [r.shape for r in recs] == [(5, 16), (1, 16), (3, 16)]
+    best = PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT)
+    small = OracleBackedRing(16 * 30, 64)     # 480 B: request 1 alone fits
+    plan = prepare_step(best, batch, small, reg, step_seq=1, ragged=True)
+    assert plan.kept_ids == (1,) and plan.dropped_ids == (2, 3)
+    bad = install_hooks(ModelSpec(1, 16), [HookSpec(
+        "attn", (4, "tokens", "tokens"), DType.of("bf16"), per_layer=True)])
+    with pytest.raises(ConfigError):
+        prepare_step(PolicyConfig(), batch, ring, bad, step_seq=0, ragged=True)
+
+
 def test_binary_prefix_search_equals_linear_scan():
     """The policy's binary search over kept prefixes returns what the
     reference's linear scan (policy.py:135-145) returns."""
