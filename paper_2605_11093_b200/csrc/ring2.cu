@@ -1671,9 +1671,13 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
       r->meta_tail = ++tail;
       r->consumed += 1;
       advanced = true;
-      if (!(d.flags & TF_DESC_HOST_RESERVED))
+      if (!(d.flags & TF_DESC_HOST_RESERVED)) {
         r->regions.push_back(HostRegion{d.payload_offset, tf_round_up16(d.payload_len),
-                                        d.skip_before, d.flags});
+                                        d.skip_before, d.flags, true});
+      } else {
+        for (HostRegion& h : r->regions)
+          if (!h.polled && h.off == d.payload_offset) { h.polled = true; break; }
+      }
     } else {
       ++tail;
     }
@@ -1749,7 +1753,12 @@ int tf_internal_release(tf_ring* r, uint64_t offset, uint64_t length, bool push)
 uint64_t tf_internal_l_after_all(tf_ring* r) {
   std::lock_guard<std::mutex> g(r->mu);
   uint64_t L = r->L;
-  for (const HostRegion& h : r->regions) L += h.skip + h.len;
+  // stop at the first region whose descriptor the consumer has not taken:
+  // a host-reserved region may still be waiting for its payload and publish
+  for (const HostRegion& h : r->regions) {
+    if (!h.polled) break;
+    L += h.skip + h.len;
+  }
   return L;
 }
 

@@ -57,6 +57,9 @@ struct alignas(128) DevCtl {
 struct HostRegion {
   uint64_t off, len, skip;
   uint32_t kind;
+  // descriptor polled by the consumer: only a leading run of polled regions
+  // may be handed back to the device allocator ahead of its release
+  bool polled = false;
 };
 
 struct tf_ring {

@@ -1,0 +1,100 @@
+"""Capture-kernel size sweep: per-launch time of N back-to-back captures
+replayed as a CUDA graph into an empty ring (staging idle), against a
+plain D2D copy of the same bytes (torch copy_ and cudaMemcpyAsync) in the
+same graph shape. Separates fixed per-launch cost from the bandwidth slope.
+
+usage: python scripts/exp_sweep.py [--n 16] [--sizes-mib 1,4,16,32,64,112,224]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_11093_b200 import DrainConfig, ExportPipeline, RingConfig, RingPair  # noqa: E402
+from paper_2605_11093_b200.hooks import RowSource, capture_args, launch_capture  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=16)
+ap.add_argument("--sizes-mib", default="1,4,16,32,64,112,224")
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--out", default="gpurun_out/sweep.json")
+args = ap.parse_args()
+
+dev = torch.device("cuda:0")
+torch.cuda.set_device(dev)
+PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6545.9
+B = 8
+res = []
+ring = RingPair(RingConfig(payload_capacity=24 << 30, meta_slots=4096), device=0)
+pipe = ExportPipeline(ring, DrainConfig(min_ready_entries=1, min_ready_bytes=1, max_wait=1e-4,
+                                        staging_buffer_size=256 << 20, staging_buffer_count=4,
+                                        discard_paged=True))
+keep = torch.ones(B, dtype=torch.uint8, device=dev)
+s = torch.cuda.Stream()
+
+
+def drain():
+    pipe.start(sink=None)
+    pipe.flush(300)
+    pipe.stop(flush=True)
+
+
+def timed_graph(fn, reps):
+    with torch.cuda.stream(s):
+        fn()  # warm
+    s.synchronize()
+    drain()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    out = []
+    for _ in range(reps):
+        drain()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record()
+            g.replay()
+            e1.record()
+        s.synchronize()
+        out.append(e0.elapsed_time(e1) * 1e3 / args.n)
+    del g
+    drain()
+    return statistics.median(out)
+
+
+for mib in [int(x) for x in args.sizes_mib.split(",")]:
+    nbytes = mib << 20
+    row = nbytes // B
+    xs = [torch.empty(nbytes, dtype=torch.uint8, device=dev).random_() for _ in range(min(args.n, 4))]
+    dsts = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(min(args.n, 4))]
+    caps = []
+    for i in range(args.n):
+        x = xs[i % len(xs)]
+        src = RowSource(x.data_ptr(), B, 1, row, row, row, x)
+        caps.append(capture_args(src, hook_id=i, keep_ptr=keep.data_ptr(), keep_per_outer=True,
+                                 step_seq=0, full="wait"))
+
+    def cap_step():
+        for a in caps:
+            launch_capture(ring, a, s)
+
+    def copy_step():
+        for i in range(args.n):
+            dsts[i % len(dsts)].copy_(xs[i % len(xs)])
+
+    t_cap = timed_graph(cap_step, args.reps)
+    t_copy = timed_graph(copy_step, args.reps)
+    ideal = 2 * nbytes / (PEAK * 1e9) * 1e6
+    r = {"mib": mib, "capture_us": t_cap, "torch_copy_us": t_copy, "ideal_us": ideal,
+         "capture_frac": ideal / t_cap, "copy_frac": ideal / t_copy}
+    print(json.dumps(r), flush=True)
+    res.append(r)
+    del xs, dsts, caps
+os.makedirs(os.path.dirname(args.out), exist_ok=True)
+json.dump(res, open(args.out, "w"), indent=1)
+pipe.close()
+ring.close()
