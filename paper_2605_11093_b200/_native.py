@@ -9,6 +9,7 @@ first call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -216,9 +217,13 @@ def lib() -> C.CDLL:
             return _lib
         from . import build_ext
         build_ext.build()  # no-op unless sources are newer than the .so
-        if not _LIB_PATH.exists():  # pragma: no cover - build raises first
-            raise RuntimeError(f"native library missing: {_LIB_PATH}")
-        handle = C.CDLL(str(_LIB_PATH))
+        path = _LIB_PATH
+        variant = os.environ.get("TF_LIB_VARIANT")
+        if variant:  # experiment builds (build_ext --variant=trace)
+            path = _LIB_PATH.with_name(f"libring2_{variant}.so")
+        if not path.exists():  # pragma: no cover - build raises first
+            raise RuntimeError(f"native library missing: {path}")
+        handle = C.CDLL(str(path))
         for name, res, args in _SIGS:
             fn = getattr(handle, name)
             fn.restype = res

@@ -45,16 +45,27 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > built for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the sources to objects and link the shared library."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False,
+          variant: str | None = None) -> Path:
+    """Compile the sources to objects and link the shared library.
+
+    ``variant="trace"`` builds ``libring2_trace.so`` with -DTF_TRACE (phase
+    timers in the capture kernel) for experiments; the product library is
+    always the plain ``libring2.so``."""
+    lib = LIB if not variant else LIB_DIR / f"libring2_{variant}.so"
+    if not force and not variant and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
     nvcc = _nvcc()
     objs = []
+    defines = []
+    if variant and variant.startswith("trace"):
+        defines.append("-DTF_TRACE")
+        if variant.startswith("trace_abl"):  # trace_ablN: ablation N
+            defines.append(f"-DTF_ABL={int(variant[9:])}")
     for src in SOURCES:
-        obj = LIB_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c",
+        obj = LIB_DIR / (Path(src).stem + (f"_{variant}" if variant else "") + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", str(ROOT / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -62,18 +73,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(res.stderr)
-        (LIB_DIR / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
+        if not variant:
+            (LIB_DIR / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            *objs, "-o", str(tmp), "-Xcompiler", "-pthread", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    print(build(force="--force" in sys.argv, verbose=True, variant=var))

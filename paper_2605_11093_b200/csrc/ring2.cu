@@ -128,6 +128,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Phase tracing of the capture kernel (experiment builds only, -DTF_TRACE):
+// thread 0 of every CTA keeps its entry / offset-known / copy-done times in
+// registers and stores them (plain stores, no contention) into a per-launch
+// slot chosen by the capture sequence; the last CTA adds its publish time.
+#ifdef TF_TRACE
+constexpr int kTrLaunches = 64, kTrCtas = 1024;
+__device__ unsigned long long g_stamp[kTrLaunches][kTrCtas][6];
+__device__ unsigned long long g_pub[kTrLaunches][2];  // publish time, grid size
+#endif
+
 // streaming loads: source activations are read exactly once
 template <int VW> struct VecT;
 template <> struct VecT<16> { using T = uint4; };
@@ -284,6 +294,12 @@ struct CapParams {
 
 enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
 
+// producer snapshot values (ring2_internal.h ProdSnap)
+struct SnapVals {
+  tf_pstate p;
+  uint64_t mh, cseq, L, mt, L_phys, used, head, tail;
+};
+
 struct CapShared {
   uint32_t warp_sums[kWarps];
   uint32_t total;
@@ -291,6 +307,11 @@ struct CapShared {
   uint64_t off;
   uint32_t is_last;
   uint32_t publish;
+  uint32_t fast, fast_kind;   // fast-path plan (identical in every CTA)
+  uint64_t fast_skip, fast_mh, fast_seq;
+  tf_pstate fast_p;
+  uint64_t old_L, old_L_phys, old_head;  // snapshot inputs of the fast plan
+  SnapVals next;                          // last CTA: the next snapshot
   uint64_t desc[8];
   uint64_t* slot;
   uint32_t table[kTableMax];
@@ -299,6 +320,22 @@ struct CapShared {
 __device__ __forceinline__ uint32_t count_nonzero_bytes(uint32_t w) {
   uint32_t nz = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
   return __popc(nz);
+}
+__device__ __forceinline__ uint32_t count_nonzero16(uint4 g) {
+  return count_nonzero_bytes(g.x) + count_nonzero_bytes(g.y) + count_nonzero_bytes(g.z) +
+         count_nonzero_bytes(g.w);
+}
+
+// keep[u, min(u+16, u1)) as 16 bytes (zero past u1): one 16-B load when the
+// vector is aligned and the group is whole, else 16 independent predicated
+// byte loads (issued together, one memory latency).
+__device__ __forceinline__ uint4 load_keep16(const uint8_t* keep, int64_t u, int64_t u1, int vec) {
+  if (vec && u + 16 <= u1) return *reinterpret_cast<const uint4*>(keep + u);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (u + k < u1) w[k >> 2] |= uint32_t(keep[u + k] != 0) << (8 * (k & 3));
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // Block-wide exclusive scan of one u32 per thread; returns the exclusive
@@ -402,6 +439,181 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
   }
 }
 
+__device__ __forceinline__ ulonglong2 ld_cg_v2(const uint64_t* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.cg.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+// Rewrite the snapshot replicas (ring2_internal.h ProdSnap); lanes
+// [0, nlanes) of the caller's group share the work.
+__device__ __forceinline__ void write_snap(DevCtl* c, const SnapVals& v, int lane, int nlanes) {
+  for (int r = lane; r < kSnapReplicas; r += nlanes) {
+    ProdSnap* q = &c->snap[r];
+    q->V = v.p.V;
+    q->reset_mark = v.p.reset_mark;
+    q->reset_credit = v.p.reset_credit;
+    q->meta_head = v.mh;
+    q->L = v.L;
+    q->meta_tail = v.mt;
+    q->capture_seq = v.cseq;
+    q->L_phys = v.L_phys;
+    q->used = v.used;
+    q->head = v.head;
+    q->tail = v.tail;
+  }
+}
+
+// Single thread, after any slow-path producer operation: snapshot the
+// canonical state and the live consumer cursors (full 64-bit arithmetic).
+__device__ void write_snap_ctl(const CapParams& P) {
+  DevCtl* c = P.ctl;
+  SnapVals v;
+  v.p = c->p;
+  v.mh = c->meta_head;
+  v.cseq = c->capture_seq;
+  v.L = ld_relaxed_gpu(&P.dcons->L);
+  v.mt = ld_relaxed_gpu(&P.dcons->meta_tail);
+  v.L_phys = v.L % P.cap;
+  v.used = tf_used(&v.p, v.L);
+  v.head = tf_head(&v.p, P.cap);
+  v.tail = tf_tail(&v.p, v.L, P.cap);
+  write_snap(c, v, 0, 1);
+}
+
+// x mod m through the 32-bit unit when both fit
+__device__ __forceinline__ uint64_t umod64(uint64_t x, uint64_t m) {
+  if ((x | m) >> 32 == 0) return (uint32_t)x % (uint32_t)m;
+  return x % m;
+}
+
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+struct SnapRegs {  // a={V,mark} b={credit,mh} l={L,mt} e={cseq,L_phys} u={used,head} t={tail,-}
+  ulonglong2 a, b, l, e, u, t;
+};
+__device__ __forceinline__ void snap_load(const CapParams& P, SnapRegs& r) {
+  const ProdSnap* q = &P.ctl->snap[blockIdx.x % kSnapReplicas];
+  r.a = ld_cg_v2(&q->V);
+  r.b = ld_cg_v2(&q->reset_credit);
+  r.l = ld_cg_v2(&q->L);
+  r.e = ld_cg_v2(&q->capture_seq);
+  r.u = ld_cg_v2(&q->used);
+  r.t = ld_cg_v2(&q->tail);
+}
+__device__ __forceinline__ bool fast_plan(const CapParams& P, const SnapRegs& r, uint64_t bytes,
+                                          CapShared& sh) {
+  const uint64_t len = tf_round_up16(bytes);
+  if (len > P.cap) return false;
+  const uint64_t mh = r.b.y, mt = r.l.y;
+  if (mh - mt >= P.slots) return false;
+  tf_pstate p;
+  p.V = r.a.x;
+  p.reset_mark = r.a.y;
+  p.reset_credit = r.b.x;
+  uint64_t off, skip;
+  uint32_t kind;
+  if (!tf_reserve_derived(&p, r.l.x, P.cap, len, r.u.x, r.u.y, r.t.x, &off, &skip, &kind))
+    return false;
+  sh.fast_p = p;
+  sh.off = off;
+  sh.fast_skip = skip;
+  sh.fast_kind = kind;
+  sh.fast_mh = mh;
+  sh.fast_seq = r.e.x + 1;
+  sh.old_L = r.l.x;
+  sh.old_L_phys = r.e.y;
+  sh.old_head = r.u.y;
+  return true;
+}
+
+// Last CTA of a fast-path launch, thread 0: the descriptor, the result
+// record and the canonical state, all stores. Its inputs were loaded before
+// the done count (step number, consumer cursors), so nothing here waits on
+// memory.
+__device__ void fast_finish(const CapParams& P, CapShared& sh, uint64_t bytes, uint64_t rows,
+                            uint32_t step, uint64_t L, uint64_t mt, uint64_t k0) {
+  DevCtl* c = P.ctl;
+  const uint64_t len = tf_round_up16(bytes), seq = sh.fast_seq;
+  tf_descriptor d;
+  d.payload_offset = sh.off;
+  d.payload_len = bytes;
+  d.hook_id = P.hook_id;
+  d.step_seq = step;
+  d.ready_seq = TF_READY_SENTINEL;
+  d.skip_before = sh.fast_skip;
+  d.flags = sh.fast_kind;
+  d.n_rows = (uint32_t)rows;
+  d.capture_seq = seq;
+  d.checksum = 0;
+  uint64_t mh = sh.fast_mh;
+  sh.publish = 0;
+  if (!(P.flags & TF_CAP_DEFER_PUBLISH)) {
+    d.ready_seq = mh;
+    d.checksum = tf_desc_checksum(reinterpret_cast<const uint64_t*>(&d));
+    sh.slot = reinterpret_cast<uint64_t*>(P.meta + umod64(mh, P.slots) * TF_DESCRIPTOR_SIZE);
+    sh.publish = 1;
+    mh += 1;
+  }
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(&d);
+  for (int i = 0; i < 8; ++i) sh.desc[i] = w[i];
+  // next snapshot, derived incrementally (skip + len <= cap and
+  // L - old_L <= cap, so one conditional subtraction replaces each modulo)
+  {
+    const uint64_t cap = P.cap;
+    SnapVals& v = sh.next;
+    v.p = sh.fast_p;
+    v.mh = mh;
+    v.cseq = seq;
+    v.mt = mt;
+    if (L < sh.old_L) L = sh.old_L;
+    v.L = L;
+    uint64_t lp = sh.old_L_phys + (L - sh.old_L);
+    if (L - sh.old_L > cap) lp = L % cap;
+    else if (lp >= cap) lp -= cap;
+    v.L_phys = lp;
+    uint64_t h = sh.old_head + sh.fast_skip + len;
+    if (h >= cap) h -= cap;
+    v.head = h;
+    const uint64_t credit = tf_credit(&v.p, L);
+    v.used = v.p.V - L - credit;
+    uint64_t t = lp + credit;
+    if (t >= cap) t -= cap;
+    v.tail = t;
+  }
+  c->p = sh.fast_p;
+  c->meta_head = mh;
+  c->capture_seq = seq;
+  c->plan_seq = seq;
+  c->plan_bytes = bytes;
+  c->plan_rows = rows;
+  c->plan_len = len;
+  c->plan_off = sh.off;
+  c->plan_skip = sh.fast_skip;
+  c->plan_kind = sh.fast_kind;
+  c->plan_status = TF_OK;
+  tf_capture_result& r = c->res;
+  r.capture_seq = seq;
+  r.status = TF_OK;
+  r.n_rows = (uint32_t)rows;
+  r.payload_offset = sh.off;
+  r.payload_len = bytes;
+  r.skip_before = sh.fast_skip;
+  r.ready_seq = d.ready_seq;
+  r.desc = d;
+  atomicAdd((unsigned long long*)&c->captures, 1ull);
+  atomicAdd((unsigned long long*)&c->bytes_reserved, (unsigned long long)len);
+  if (sh.fast_kind & TF_DESC_DEAD_SKIP)
+    atomicAdd((unsigned long long*)&c->dead_created, (unsigned long long)sh.fast_skip);
+  const uint64_t dt = globaltimer() - k0;
+  c->last_kernel_ns = dt;
+  atomicAdd((unsigned long long*)&c->kernel_ns, (unsigned long long)dt);
+}
+
 // Non-leader CTAs wait for the leader's plan with exponential backoff: under
 // completeness the leader may wait milliseconds for ring space, and a tight
 // poll of one L2 line by hundreds of CTAs taxes the memory system the
@@ -455,8 +667,15 @@ __device__ void last_cta_prepare(const CapParams& P, CapShared& sh) {
   r.desc = d;
 }
 
+// 64-bit quotient through the 32-bit divider when both operands fit (the
+// usual case: rows, segments and items of one capture are < 2^32)
+__device__ __forceinline__ int64_t qdiv(int64_t a, int64_t b) {
+  if (((uint64_t)a | (uint64_t)b) >> 32 == 0) return (int64_t)((uint32_t)a / (uint32_t)b);
+  return a / b;
+}
+
 __device__ __forceinline__ const uint8_t* row_src(const CapParams& P, int64_t row) {
-  int64_t o = row / P.mid;
+  int64_t o = qdiv(row, P.mid);
   int64_t m = row - o * P.mid;
   return P.src + o * P.s_outer + m * P.s_mid;
 }
@@ -467,27 +686,71 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t U = P.units;
   const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
+#ifdef TF_TRACE
+  uint64_t t_plan = 0, t_scan = 0, t_fast = 0, t_table = 0;
+#define TSTAMP(v) do { if (tid == 0) v = globaltimer(); } while (0)
+#else
+#define TSTAMP(v) ((void)0)
+#endif
+
+#ifndef TF_ABL
+#define TF_ABL 0
+#endif
+  // experiment builds: TF_ABL bit 1 = no keep scan, bit 2 = no publish
+  // epilogue, bit 4 = no snapshot (fixed offset 0), 8 = no descriptor post,
+  // 16 = no snapshot rewrite, 32 = no state commit
+  if (TF_ABL & 1) P.keep = nullptr;
+  // PDL: let the next kernel on the stream get scheduled now; it still waits
+  // for this grid's completion before touching memory. Then wait for the
+  // previous kernel (it may have produced the source rows, and the previous
+  // capture wrote the producer snapshot). No-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Issue the producer-snapshot and step loads first: their latency hides
+  // behind the keep scan (step is consumed only by the publishing CTA).
+  SnapRegs sr;
+  uint32_t step = 0;
+  if (tid == 0 && !(TF_ABL & 4)) {
+    snap_load(P, sr);
+    step = P.step_ptr ? *P.step_ptr : P.step_imm;
+  }
 
   // ---- 1. ordered compaction: count kept units (batch order, no atomics) ----
+  // Each thread owns a run of whole 16-unit groups; the first group stays
+  // in registers for the rank table below (one keep load per thread in the
+  // common case of <= 4096 units).
   int64_t u0 = 0, u1 = 0;
   uint32_t mycnt = 0, mybase = 0;
+  uint4 g0 = make_uint4(0u, 0u, 0u, 0u);
   uint64_t K;
-  if (P.keep) {
+  // <= 32 keep units (request keep): one warp, one coalesced load, ranks by
+  // ballot; the whole rank table is built here and indexed from rank 0
+  const bool small = P.keep && U <= 32;
+  if (small) {
+    if (warp == 0) {
+      const uint32_t k = lane < U ? P.keep[lane] : 0u;
+      const uint32_t m = __ballot_sync(0xffffffffu, k != 0);
+      if (k) sh.table[__popc(m & ((1u << lane) - 1u))] = (uint32_t)lane;
+      if (lane == 0) sh.total = __popc(m);
+    }
+    __syncthreads();
+    K = sh.total;
+    TSTAMP(t_scan);
+  } else if (P.keep) {
     int64_t per = (U + kThreads - 1) / kThreads;
-    if (P.keep_vec) per = (per + 15) & ~int64_t(15);
+    per = (per + 15) & ~int64_t(15);
     u0 = imin64(int64_t(tid) * per, U);
     u1 = imin64(u0 + per, U);
-    int64_t u = u0;
-    if (P.keep_vec) {
-      for (; u + 16 <= u1; u += 16) {
-        uint4 k = *reinterpret_cast<const uint4*>(P.keep + u);
-        mycnt += count_nonzero_bytes(k.x) + count_nonzero_bytes(k.y) +
-                 count_nonzero_bytes(k.z) + count_nonzero_bytes(k.w);
-      }
+    if (u0 < u1) {
+      g0 = load_keep16(P.keep, u0, u1, P.keep_vec);
+      mycnt = count_nonzero16(g0);
+#pragma unroll 1
+      for (int64_t u = u0 + 16; u < u1; u += 16)
+        mycnt += count_nonzero16(load_keep16(P.keep, u, u1, P.keep_vec));
     }
-    for (; u < u1; ++u) mycnt += P.keep[u] != 0;
     mybase = block_exclusive_scan(mycnt, sh);
     K = sh.total;
+    TSTAMP(t_scan);
   } else {
     K = (uint64_t)U;
   }
@@ -505,16 +768,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
   const uint64_t out_bytes = n_rows * (uint64_t)P.out_row_bytes;
 
-  // ---- 2. leader election; reservation runs while the others prefetch ----
-  bool leader = false;
+  // ---- 2. reservation: fast path in every CTA, else leader election ----
+  // (the leader's reservation runs while the others prefetch)
+  bool leader = false, fast = false;
   if (tid == 0) {
-    uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
-    leader = (t == 0);
-    if (leader) {
-      P.ctl->k_t0 = t_entry;
-      leader_reserve(P, out_bytes, n_rows);
-      __threadfence();
-      st_release_gpu(&P.ctl->plan_flag, 1u);
+    if (TF_ABL & 4) {
+      fast = true;
+      sh.off = 0;
+    } else {
+      fast = fast_plan(P, sr, out_bytes, sh);
+    }
+    sh.fast = fast;
+    TSTAMP(t_fast);
+    if (fast) {
+      sh.status = TF_OK;
+    } else {
+      uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
+      leader = (t == 0);
+      if (leader) {
+        P.ctl->k_t0 = t_entry;
+        leader_reserve(P, out_bytes, n_rows);
+        __threadfence();
+        st_release_gpu(&P.ctl->plan_flag, 1u);
+      }
     }
   }
 
@@ -526,29 +802,36 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     spr = (P.words_per_row + kSeg - 1) / kSeg;
     items = (int64_t)n_rows * spr;
   }
-  const int64_t chunk = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t chunk = qdiv(items + gridDim.x - 1, gridDim.x);
   const int64_t i0 = imin64(int64_t(blockIdx.x) * chunk, items);
   const int64_t i1 = imin64(i0 + chunk, items);
-  const int64_t j_lo = i0 / spr;
-  const int64_t r_lo = j_lo / P.rpu;
-  if (P.keep && i0 < i1) {
-    const int64_t r_hi = ((i1 - 1) / spr) / P.rpu;
+  const int64_t j_lo = qdiv(i0, spr);
+  const int64_t r_lo = qdiv(j_lo, P.rpu);
+  const int64_t tbase = small ? 0 : r_lo;  // rank of sh.table[0]
+  if (P.keep && !small && i0 < i1) {
+    const int64_t r_hi = qdiv(qdiv(i1 - 1, spr), P.rpu);
     // rank -> unit table for the ranks this CTA touches
     if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
       int64_t rank = mybase;
-      for (int64_t u = u0; u < u1 && rank <= r_hi; ++u) {
-        if (P.keep[u]) {
-          if (rank >= r_lo) sh.table[rank - r_lo] = (uint32_t)u;
-          ++rank;
+      for (int64_t u = u0; u < u1 && rank <= r_hi; u += 16) {
+        const uint4 g = u == u0 ? g0 : load_keep16(P.keep, u, u1, P.keep_vec);
+        const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if ((gw[k >> 2] >> (8 * (k & 3))) & 0xFFu) {
+            if (rank >= r_lo && rank <= r_hi) sh.table[rank - r_lo] = (uint32_t)(u + k);
+            ++rank;
+          }
         }
       }
     }
   }
   __syncthreads();
+  TSTAMP(t_table);
   auto row_of = [&](int64_t j) -> int64_t {
-    int64_t r = j / P.rpu;
+    int64_t r = qdiv(j, P.rpu);
     int64_t sub = j - r * P.rpu;
-    int64_t unit = P.keep ? (int64_t)sh.table[r - r_lo] : r;
+    int64_t unit = P.keep ? (int64_t)sh.table[r - tbase] : r;
     return unit * P.rpu + sub;
   };
 
@@ -560,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     V v[kUnroll];
     int64_t k0 = 0, k1 = 0, j = 0;
     if (s < i1) {
-      j = s / spr;
+      j = qdiv(s, spr);
       k0 = (s - j * spr) * kSeg;
       k1 = imin64(k0 + kSeg, wpr);
       const uint8_t* src = row_src(P, row_of(j));
@@ -570,13 +853,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
       }
     }
-    if (tid == 0) {
-      if (!leader)
-        wait_plan(P.ctl);
-      sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
-      sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+    if (!sh.fast) {  // uniform: sh.fast was set before the table barrier
+      if (tid == 0) {
+        if (!leader)
+          wait_plan(P.ctl);
+        sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
+        sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
+      }
+      __syncthreads();
     }
-    __syncthreads();
+#ifdef TF_TRACE
+    if (tid == 0) t_plan = globaltimer();
+#endif
     if (sh.status == TF_OK && s < i1) {
       uint8_t* dst_base = P.payload + sh.off;
       for (;;) {
@@ -588,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         }
         s += kWarps;
         if (s >= i1) break;
-        j = s / spr;
+        j = qdiv(s, spr);
         k0 = (s - j * spr) * kSeg;
         k1 = imin64(k0 + kSeg, wpr);
         const uint8_t* src = row_src(P, row_of(j));
@@ -600,7 +888,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       }
     }
   } else {
-    if (tid == 0) {
+    if (tid == 0 && !fast) {
       if (!leader)
         wait_plan(P.ctl);
       sh.status = *((volatile uint32_t*)&P.ctl->plan_status);
@@ -696,26 +984,57 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
 
   // ---- 4. the last CTA to retire publishes ----
+  if (TF_ABL & 2) return;
   __syncthreads();
+  uint64_t L_now = 0, mt_now = 0;
   if (tid == 0) {
-    __threadfence();  // this CTA's payload stores, gpu scope, before the count
-    uint32_t t = atomicAdd(&P.ctl->done, 1u);
+    // consumer cursors for the next snapshot, loaded while the fence and the
+    // done count are in flight (any older L is conservative)
+    L_now = ld_relaxed_gpu(&P.dcons->L);
+    mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
+#ifdef TF_TRACE
+    {
+      const int slot = sh.fast ? int(sh.fast_seq % kTrLaunches) : kTrLaunches - 1;
+      if (blockIdx.x < kTrCtas) {
+        g_stamp[slot][blockIdx.x][0] = t_entry;
+        g_stamp[slot][blockIdx.x][1] = t_plan;
+        g_stamp[slot][blockIdx.x][2] = globaltimer();
+        g_stamp[slot][blockIdx.x][3] = t_scan;
+        g_stamp[slot][blockIdx.x][4] = t_fast;
+        g_stamp[slot][blockIdx.x][5] = t_table;
+      }
+    }
+#endif
+    // release: the CTA's payload stores (ordered by the barrier above)
+    // before the count; acquire: the last CTA sees every other CTA's
+    uint32_t t = atom_add_acqrel_gpu(&P.ctl->done, 1u);
     sh.is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (sh.is_last) {
     if (tid == 0) {
-      __threadfence();
-      last_cta_prepare(P, sh);
+      if (sh.fast) {
+        if (!(TF_ABL & 32)) fast_finish(P, sh, out_bytes, n_rows, step, L_now, mt_now, t_entry);
+      } else {
+        last_cta_prepare(P, sh);
+        write_snap_ctl(P);
+      }
     }
     __syncthreads();
     // one coalesced 64-byte post of the descriptor, no system fence: the
     // host verifies the checksum before it trusts the slot
-    if (sh.publish && warp == 0 && lane < 8) sh.slot[lane] = sh.desc[lane];
+    if (!(TF_ABL & 8) && sh.publish && warp == 0 && lane < 8) sh.slot[lane] = sh.desc[lane];
+    if (!(TF_ABL & 16) && sh.fast && warp == 1)
+      write_snap(P.ctl, sh.next, lane, 32);  // next launch's snapshot
     if (tid == 0) {  // re-arm the handshake for the next launch on this stream
       P.ctl->arrive = 0;
       P.ctl->done = 0;
       P.ctl->plan_flag = 0;  // visible to the next launch (kernel boundary)
+#ifdef TF_TRACE
+      const int slot = sh.fast ? int(sh.fast_seq % kTrLaunches) : kTrLaunches - 1;
+      g_pub[slot][0] = globaltimer();
+      g_pub[slot][1] = gridDim.x;
+#endif
     }
   }
 }
@@ -919,6 +1238,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) capture_tma_kernel(CapParams P
     if (tid == 0) {
       __threadfence();
       last_cta_prepare(P, sh);
+      write_snap_ctl(P);
     }
     __syncthreads();
     if (sh.publish && tid < 8) sh.slot[tid] = sh.desc[tid];
@@ -1087,6 +1407,7 @@ __global__ void __launch_bounds__(kStgThreads, kStgCtasPerSm) capture_stage_kern
     if (tid == 0) {
       __threadfence();
       last_cta_prepare(P, sh);
+      write_snap_ctl(P);
     }
     __syncthreads();
     if (sh.publish && tid < 8) sh.slot[tid] = sh.desc[tid];
@@ -1118,6 +1439,7 @@ __global__ void reserve_kernel(CapParams P, uint64_t len) {
   c->res.payload_offset = off;
   c->res.skip_before = skip;
   c->res.payload_len = len;
+  write_snap_ctl(P);
 }
 
 __global__ void publish_kernel(CapParams P, tf_descriptor d) {
@@ -1146,6 +1468,7 @@ __global__ void publish_kernel(CapParams P, tf_descriptor d) {
   }
   c->res.ready_seq = seq;
   c->res.status = status;
+  write_snap_ctl(P);
 }
 
 }  // namespace
@@ -1232,6 +1555,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
   }
   memset(r->ctl_host, 0, sizeof(DevCtl));
   r->ctl_host->p.reset_mark = TF_NO_MARK;
+  for (int i = 0; i < kSnapReplicas; ++i) r->ctl_host->snap[i].reset_mark = TF_NO_MARK;
   if (cudaMemcpy(r->ctl, r->ctl_host, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(r->dcons, 0, sizeof(DevConsumer)) != cudaSuccess ||
       cudaMemset(r->payload, 0, cfg->payload_capacity) != cudaSuccess) {
@@ -1309,9 +1633,31 @@ extern "C" int tf_capture_out_row_bytes(const tf_capture_args* a, int64_t* out) 
   return TF_ERR_CONFIG;
 }
 
+// Programmatic dependent launch: a capture kernel may be scheduled while the
+// kernel before it on the stream drains; it waits (griddepcontrol.wait) for
+// that kernel's completion and memory before its first global access, so
+// only launch latency and CTA start-up overlap. TF_PDL=0 disables.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int MODE, int VW, int IN, int OUT>
 static int launch(const CapParams& P, int grid, cudaStream_t s) {
-  capture_kernel<MODE, VW, IN, OUT><<<grid, kThreads, 0, s>>>(P);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, capture_kernel<MODE, VW, IN, OUT>, P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     tf_set_error("capture launch: %s", cudaGetErrorString(e));
@@ -1853,3 +2199,14 @@ extern "C" int tf_ring_would_fit(tf_ring* r, const uint64_t* lengths, uint32_t n
   *fits = entries <= free_slots;
   return TF_OK;
 }
+
+#ifdef TF_TRACE
+// experiment builds: copy out the per-launch stamps ([64][1024][6] entry,
+// offset known, copy done, scan done, fast plan done, table done) and publish records ([64][2] time, grid)
+extern "C" int tf_debug_trace(unsigned long long* stamps, unsigned long long* pub) {
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(stamps, g_stamp, sizeof(g_stamp)));
+  CUDA_TRY(cudaMemcpyFromSymbol(pub, g_pub, sizeof(g_pub)));
+  return TF_OK;
+}
+#endif

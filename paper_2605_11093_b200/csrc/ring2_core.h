@@ -73,16 +73,16 @@ TF_HD uint64_t tf_tail(const tf_pstate* p, uint64_t L, uint64_t cap) {
 // rings.py:286-319 reserve_payload as a state transition on (pstate, L).
 // `skip` is the number of virtual bytes consumed before the region and
 // `kind` says whether they were a dead region or an empty-ring reset.
-TF_HD int tf_reserve(tf_pstate* p, uint64_t L, uint64_t cap, uint64_t len,
-                     uint64_t* off, uint64_t* skip, uint32_t* kind) {
-  uint64_t used = tf_used(p, L);
-  uint64_t head = tf_head(p, cap);
-  uint64_t tail = tf_tail(p, L, cap);
+// tf_reserve with (used, head, tail) of (p, L) already derived, so a caller
+// holding them precomputed skips the 64-bit modulo arithmetic.
+TF_HD int tf_reserve_derived(tf_pstate* p, uint64_t L, uint64_t cap, uint64_t len,
+                             uint64_t used, uint64_t head, uint64_t tail,
+                             uint64_t* off, uint64_t* skip, uint32_t* kind) {
   uint64_t o = 0, d = 0;
   if (!tf_plan(head, tail, used, cap, len, &o, &d)) return 0;
   if (used == 0) {
     // empty: V == L here (a pending credit implies used > 0)
-    uint64_t s = (cap - head) % cap;
+    uint64_t s = head ? cap - head : 0;
     p->reset_mark = L;
     p->reset_credit = s;
     *skip = s;
@@ -99,4 +99,10 @@ TF_HD int tf_reserve(tf_pstate* p, uint64_t L, uint64_t cap, uint64_t len,
   }
   *off = o;
   return 1;
+}
+
+TF_HD int tf_reserve(tf_pstate* p, uint64_t L, uint64_t cap, uint64_t len,
+                     uint64_t* off, uint64_t* skip, uint32_t* kind) {
+  return tf_reserve_derived(p, L, cap, len, tf_used(p, L), tf_head(p, cap),
+                            tf_tail(p, L, cap), off, skip, kind);
 }

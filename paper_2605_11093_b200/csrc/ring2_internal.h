@@ -34,6 +34,22 @@ struct alignas(128) DevConsumer {
   uint64_t pad1[15];
 };
 
+// Producer snapshot for the capture kernel's fast path: the allocator
+// state, meta head and capture sequence after the last producer operation,
+// the consumer cursors as that operation's final thread read them, and the
+// (used, head, tail) derived from them. Every kernel that moves the producer
+// state rewrites all replicas before it exits, so the words are stable for
+// the whole next launch: each CTA reads its replica (spreading the reads of
+// hundreds of CTAs over several L2 lines), runs the allocator on the same
+// inputs and reaches the same offset with no cross-CTA handshake. L only
+// grows, so a snapshot L is conservative (it never hands out live bytes).
+struct alignas(128) ProdSnap {
+  uint64_t V, reset_mark, reset_credit, meta_head;
+  uint64_t L, meta_tail, capture_seq, L_phys;  // L_phys = L % capacity
+  uint64_t used, head, tail, pad1[5];
+};
+constexpr int kSnapReplicas = 8;
+
 struct alignas(128) DevCtl {
   // allocator (producer role)
   tf_pstate p;
@@ -46,12 +62,14 @@ struct alignas(128) DevCtl {
   uint32_t arrive, done, plan_flag, plan_status;
   uint64_t plan_off, plan_skip, plan_len, plan_bytes, plan_rows, plan_seq;
   uint32_t plan_kind, pad0;
+
   // device-side timing of capture kernels (globaltimer, ns)
   uint64_t k_t0, kernel_ns, last_kernel_ns;
   uint64_t pad1;
   // result of the most recent launch (device memory; the host copies the
   // whole block on a side stream when it needs a snapshot)
   tf_capture_result res;
+  ProdSnap snap[kSnapReplicas];
 };
 
 struct HostRegion {
