@@ -828,6 +828,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
   __syncthreads();
   TSTAMP(t_table);
+  // Work order. With a global rank table (small keep, or no keep) the warps
+  // of all CTAs walk the segments grid-interleaved, so at any moment the
+  // active reads and writes cover one contiguous window of the source and
+  // the ring (DRAM page locality, like a grid-stride copy); otherwise each
+  // CTA walks its own contiguous slice [i0, i1) whose ranks its table holds.
+  const bool inter = (small || !P.keep) && !(TF_ABL & 64);
+  const int64_t s_first = inter ? int64_t(blockIdx.x) * kWarps + warp : i0 + warp;
+  const int64_t s_step = inter ? int64_t(gridDim.x) * kWarps : kWarps;
+  const int64_t s_end = inter ? items : i1;
   auto row_of = [&](int64_t j) -> int64_t {
     int64_t r = qdiv(j, P.rpu);
     int64_t sub = j - r * P.rpu;
@@ -839,10 +848,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     using V = typename VecT<VW>::T;
     const int64_t wpr = P.words_per_row;
     // prefetch this warp's first segment before the offset is known
-    int64_t s = i0 + warp;
+    int64_t s = s_first;
     V v[kUnroll];
     int64_t k0 = 0, k1 = 0, j = 0;
-    if (s < i1) {
+    if (s < s_end) {
       j = qdiv(s, spr);
       k0 = (s - j * spr) * kSeg;
       k1 = imin64(k0 + kSeg, wpr);
@@ -865,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #ifdef TF_TRACE
     if (tid == 0) t_plan = globaltimer();
 #endif
-    if (sh.status == TF_OK && s < i1) {
+    if (sh.status == TF_OK && s < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
       for (;;) {
         uint8_t* dst = dst_base + j * P.out_row_bytes;
@@ -874,8 +883,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           int64_t k = k0 + lane + i * 32;
           if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
         }
-        s += kWarps;
-        if (s >= i1) break;
+        s += s_step;
+        if (s >= s_end) break;
         j = qdiv(s, spr);
         k0 = (s - j * spr) * kSeg;
         k1 = imin64(k0 + kSeg, wpr);
@@ -895,13 +904,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       sh.off = *((volatile uint64_t*)&P.ctl->plan_off);
     }
     __syncthreads();
-    if (sh.status == TF_OK && i0 < i1) {
+    if (sh.status == TF_OK && s_first < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
       if constexpr (MODE == MODE_CAST) {
         // VW == 8: groups of 8 elements; VW == 1: single elements
         constexpr int WI = Elem<IN_DT>::W, WO = Elem<OUT_DT>::W;
         const int64_t wpr = P.words_per_row;
-        for (int64_t s = i0 + warp; s < i1; s += kWarps) {
+        for (int64_t s = s_first; s < s_end; s += s_step) {
           const int64_t j = s / spr;
           const int64_t k0 = (s - j * spr) * kSeg;
           const int64_t k1 = imin64(k0 + kSeg, wpr);
@@ -928,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         // MODE_REDUCE: one warp per row, fp64 accumulation, f32 outputs
         constexpr int WI = Elem<IN_DT>::W;
         const int64_t H = P.row_elems;
-        for (int64_t j = i0 + warp; j < i1; j += kWarps) {
+        for (int64_t j = s_first; j < s_end; j += s_step) {
           const uint8_t* src = row_src(P, row_of(j));
           double sum = 0.0, sq = 0.0;
           float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
@@ -1741,10 +1750,19 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (a->mid > 1) sal = std::min(sal, pow2_align((uint64_t)a->stride_mid));
   const int64_t total_rows = a->outer * a->mid;
   const uint64_t out_max = uint64_t(total_rows) * uint64_t(orb);
-  // grid: one 16 KiB chunk per CTA up to kCtasPerSm CTAs per SM (all
-  // resident, so the spin on the leader's plan can never starve it)
-  int grid_bytes = int(std::min<uint64_t>((out_max + (16u << 10) - 1) / (16u << 10),
-                                          uint64_t(g_sm_count) * kCtasPerSm));
+  // grid: one chunk (default 16 KiB) per CTA up to `waves` x kCtasPerSm
+  // CTAs per SM. The leader of a slow-path launch is the first CTA to
+  // arrive, so CTAs that become resident later never starve it.
+  static int chunk_kb = -1, waves = -1;
+  if (chunk_kb < 0) {
+    const char* e = getenv("TF_CAP_CHUNK_KB");
+    chunk_kb = e ? std::max(1, atoi(e)) : 16;
+    e = getenv("TF_CAP_WAVES");
+    waves = e ? std::max(1, atoi(e)) : 1;
+  }
+  const uint64_t chunk = uint64_t(chunk_kb) << 10;
+  int grid_bytes = int(std::min<uint64_t>((out_max + chunk - 1) / chunk,
+                                          uint64_t(g_sm_count) * kCtasPerSm * waves));
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
   int grid = std::max(1, std::max(grid_bytes, grid_table));
   if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));
