@@ -61,8 +61,11 @@ def build(force: bool = False, verbose: bool = False,
     defines = []
     if variant and variant.startswith("trace"):
         defines.append("-DTF_TRACE")
-        if variant.startswith("trace_abl"):  # trace_ablN: ablation N
-            defines.append(f"-DTF_ABL={int(variant[9:])}")
+        for part in variant.split("_")[1:]:  # trace_ablN_cM: ablation N, M CTAs/SM
+            if part.startswith("abl"):
+                defines.append(f"-DTF_ABL={int(part[3:])}")
+            elif part.startswith("c"):
+                defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")
     for src in SOURCES:
         obj = LIB_DIR / (Path(src).stem + (f"_{variant}" if variant else "") + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", str(ROOT / "include"), "-c",

@@ -168,7 +168,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTableMax = 2048;
 constexpr int kUnroll = 8;
 constexpr int kSeg = 32 * kUnroll;  // vector words per warp segment
-constexpr int kCtasPerSm = 3;
+#ifndef TF_CTAS_PER_SM
+#define TF_CTAS_PER_SM 2
+#endif
+constexpr int kCtasPerSm = TF_CTAS_PER_SM;
 
 // ---------------------------------------------------------------------------
 // element conversions (bit-exact with oracle/cast_oracle.c)
@@ -714,6 +717,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     snap_load(P, sr);
     step = P.step_ptr ? *P.step_ptr : P.step_imm;
   }
+  // COPY: speculatively load this warp's first segment of the
+  // grid-interleaved order assuming every unit is kept (identity row map),
+  // so the source read overlaps the keep/snapshot round trip; used only if
+  // the keep scan confirms it.
+  using CV = typename VecT<MODE == MODE_COPY ? VW : 16>::T;
+  CV v[kUnroll];
+  int64_t spec_s = -1;
+  if constexpr (MODE == MODE_COPY) {
+    if (!(TF_ABL & 256) && (!P.keep || U <= 32)) {
+      const int64_t spr0 = (P.words_per_row + kSeg - 1) / kSeg;
+      const int64_t s0 = int64_t(blockIdx.x) * kWarps + warp;
+      if (s0 < U * P.rpu * spr0) {
+        const int64_t j0 = qdiv(s0, spr0);
+        const int64_t k0 = (s0 - j0 * spr0) * kSeg;
+        const int64_t k1 = imin64(k0 + kSeg, P.words_per_row);
+        const uint8_t* src = row_src(P, j0);
+#pragma unroll
+        for (int i = 0; i < kUnroll; ++i) {
+          int64_t k = k0 + lane + i * 32;
+          if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+        }
+        spec_s = s0;
+      }
+    }
+  }
 
   // ---- 1. ordered compaction: count kept units (batch order, no atomics) ----
   // Each thread owns a run of whole 16-unit groups; the first group stays
@@ -845,21 +873,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   };
 
   if constexpr (MODE == MODE_COPY) {
-    using V = typename VecT<VW>::T;
     const int64_t wpr = P.words_per_row;
-    // prefetch this warp's first segment before the offset is known
+    // first segment: the speculative load when every unit was kept, else
+    // load it now (before the offset is known on the slow path)
     int64_t s = s_first;
-    V v[kUnroll];
     int64_t k0 = 0, k1 = 0, j = 0;
     if (s < s_end) {
       j = qdiv(s, spr);
       k0 = (s - j * spr) * kSeg;
       k1 = imin64(k0 + kSeg, wpr);
-      const uint8_t* src = row_src(P, row_of(j));
+      if (!(spec_s == s && K == (uint64_t)U)) {
+        const uint8_t* src = row_src(P, row_of(j));
 #pragma unroll
-      for (int i = 0; i < kUnroll; ++i) {
-        int64_t k = k0 + lane + i * 32;
-        if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+        for (int i = 0; i < kUnroll; ++i) {
+          int64_t k = k0 + lane + i * 32;
+          if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+        }
       }
     }
     if (!sh.fast) {  // uniform: sh.fast was set before the table barrier

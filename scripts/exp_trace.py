@@ -25,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--sizes-mib", default="1,8,32,112")
 ap.add_argument("--batch", type=int, default=8)
+ap.add_argument("--rows", type=int, default=1, help="rows per batch element (T)")
 args = ap.parse_args()
 
 lib = N.lib()
@@ -77,10 +78,11 @@ def drain():
 
 for mib in [int(x) for x in args.sizes_mib.split(",")]:
     nbytes = mib << 20
-    row = nbytes // B
+    T = args.rows
+    row = nbytes // (B * T)
     nsrc = max(1, min(args.n, (1 << 30) // nbytes))
     xs = [torch.empty(nbytes, dtype=torch.uint8, device=dev).random_() for _ in range(nsrc)]
-    caps = [capture_args(RowSource(xs[i % nsrc].data_ptr(), B, 1, row, row, row, xs[i % nsrc]),
+    caps = [capture_args(RowSource(xs[i % nsrc].data_ptr(), B, T, row, row * T, row, xs[i % nsrc]),
                          hook_id=i, keep_ptr=keep.data_ptr(), keep_per_outer=True,
                          step_seq=0, full="wait") for i in range(args.n)]
     with torch.cuda.stream(s):
