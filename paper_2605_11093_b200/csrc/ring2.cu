@@ -166,7 +166,10 @@ __device__ __forceinline__ void st_vec(uint8_t* p, typename VecT<VW>::T v) {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTableMax = 2048;
-constexpr int kUnroll = 8;
+#ifndef TF_UNROLL
+#define TF_UNROLL 8
+#endif
+constexpr int kUnroll = TF_UNROLL;
 constexpr int kSeg = 32 * kUnroll;  // vector words per warp segment
 #ifndef TF_CTAS_PER_SM
 #define TF_CTAS_PER_SM 2
