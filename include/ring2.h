@@ -347,6 +347,43 @@ int tf_measure_d2h(int device, uint64_t nbytes, int reps, double* gbps);
 /* Wall-clock of monotonic seconds (same clock the stager uses). */
 double tf_monotonic(void);
 
+/* ---- native record sinks (SRC/sinks.py:35-136 formats) ----------------
+ * Replace FileSink.write / StreamSink.write (SRC/sinks.py:53-66, 117-126)
+ * for the exporter's hot path: one call per batch of captures, each
+ * capture the matched TensorMeta (SRC/records.py:22-60) plus its payload in
+ * host memory (a staging buffer). The sink splits each payload into
+ * per-request records in batch order (SRC/exporter.py:306-327), computes
+ * zlib crc32 per record on a thread pool, formats the reference's NDJSON
+ * header byte-for-byte (fixed key order, compact separators, ASCII
+ * escapes) and writes the sidecar / frames with large writes. The calling
+ * thread never touches payload bytes in Python. */
+typedef struct tf_capture_meta {
+  const char* hook_name;        /* NUL-terminated */
+  int64_t layer;                /* -1: null */
+  int64_t step_seq;
+  int64_t tp_rank, pp_stage;
+  const char* dtype;            /* dtype name, NUL-terminated */
+  uint32_t n_req;
+  uint32_t ndim;                /* per-request shape rank (>= 1) */
+  const int64_t* request_ids;   /* n_req */
+  const int64_t* token_ranges;  /* 2 * n_req: [start, end) pairs */
+  const int64_t* row_counts;    /* n_req (ragged: shape[0] per request) or NULL */
+  const int64_t* shape;         /* ndim: per-request shape (uniform case) */
+  int64_t row_bytes;            /* bytes per shape[0] row */
+  const uint8_t* payload;       /* host memory, payload_len bytes */
+  uint64_t payload_len;
+} tf_capture_meta;
+
+typedef struct tf_sink tf_sink;
+/* records.ndjson + records.bin in `dir` (appended, like FileSink). */
+int tf_sink_open_dataset(const char* dir, uint32_t threads, tf_sink** out);
+/* u32-LE framed (header, payload) records on an open file descriptor. */
+int tf_sink_open_stream(int fd, uint32_t threads, tf_sink** out);
+int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n_caps);
+int tf_sink_stats(tf_sink* s, uint64_t* records, uint64_t* bytes);
+int tf_sink_flush(tf_sink* s);   /* fsync-free: data handed to the kernel */
+int tf_sink_close(tf_sink* s);   /* closes the files it opened, not a caller fd */
+
 #ifdef __cplusplus
 }
 #endif

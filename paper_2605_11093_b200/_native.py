@@ -76,6 +76,18 @@ class CDescriptor(C.Structure):
                 ("capture_seq", C.c_uint64), ("checksum", C.c_uint64)]
 
 
+class CCaptureMeta(C.Structure):
+    """tf_capture_meta (include/ring2.h): one matched capture for the sinks."""
+    _fields_ = [("hook_name", C.c_char_p), ("layer", C.c_int64),
+                ("step_seq", C.c_int64), ("tp_rank", C.c_int64),
+                ("pp_stage", C.c_int64), ("dtype", C.c_char_p),
+                ("n_req", C.c_uint32), ("ndim", C.c_uint32),
+                ("request_ids", C.c_void_p), ("token_ranges", C.c_void_p),
+                ("row_counts", C.c_void_p), ("shape", C.c_void_p),
+                ("row_bytes", C.c_int64), ("payload", C.c_void_p),
+                ("payload_len", C.c_uint64)]
+
+
 class CRingConfig(C.Structure):
     _fields_ = [("payload_capacity", C.c_uint64), ("meta_slots", C.c_uint32),
                 ("_pad", C.c_uint32), ("high_watermark", C.c_double),
@@ -198,6 +210,12 @@ _SIGS = [
     ("tf_free_host", None, [C.c_void_p]),
     ("tf_measure_d2h", C.c_int, [C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_double)]),
     ("tf_monotonic", C.c_double, []),
+    ("tf_sink_open_dataset", C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    ("tf_sink_open_stream", C.c_int, [C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
+    ("tf_sink_write", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
+    ("tf_sink_stats", C.c_int, [C.c_void_p, u64p, u64p]),
+    ("tf_sink_flush", C.c_int, [C.c_void_p]),
+    ("tf_sink_close", C.c_int, [C.c_void_p]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

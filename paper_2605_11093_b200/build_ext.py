@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libring2.so"
-SOURCES = ["ring2.cu", "stager.cu"]
+SOURCES = ["ring2.cu", "stager.cu", "sink.cpp"]
 HEADERS = ["ring2_core.h", "ring2_internal.h"]
 
 NVCC_FLAGS = [
@@ -83,7 +83,7 @@ def build(force: bool = False, verbose: bool = False,
         objs.append(str(obj))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-           *objs, "-o", str(tmp), "-Xcompiler", "-pthread", "-lpthread"]
+           *objs, "-o", str(tmp), "-Xcompiler", "-pthread", "-lpthread", "-lz"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

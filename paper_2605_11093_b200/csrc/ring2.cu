@@ -1537,10 +1537,22 @@ static CapParams base_params(tf_ring* r) {
 
 // Copy the device control block to the pinned snapshot (control stream:
 // never waits for the inference stream). Callers fence the producer first.
+// Snapshot of the device control block for the host. A one-CTA kernel on a
+// high-priority stream stores it into the host-mapped copy: a D2H memcpy
+// would queue on the copy engine behind the staging engine's 128 MiB
+// transfers (milliseconds per policy decision while PCIe is busy).
+__global__ void snapshot_kernel(const uint64_t* __restrict__ src, uint64_t* dst, int words) {
+  for (int i = threadIdx.x; i < words; i += blockDim.x)
+    dst[i] = ld_relaxed_gpu(src + i);
+}
+
 static int snapshot(tf_ring* r) {
-  CUDA_TRY(cudaMemcpyAsync(r->ctl_host, r->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost,
-                           (cudaStream_t)r->ctrl_stream));
-  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->ctrl_stream));
+  constexpr int words = int(sizeof(DevCtl) / 8);
+  snapshot_kernel<<<1, 256, 0, (cudaStream_t)r->snap_stream>>>(
+      reinterpret_cast<const uint64_t*>(r->ctl), reinterpret_cast<uint64_t*>(r->ctl_host_dev),
+      words);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)r->snap_stream));
   return TF_OK;
 }
 
@@ -1581,7 +1593,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
   }
   size_t meta_bytes = size_t(cfg->meta_slots) * TF_DESCRIPTOR_SIZE;
   if (cudaHostAlloc((void**)&r->meta, meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
-      cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable) != cudaSuccess) {
+      cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
     tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_ALLOCATION);
   }
@@ -1609,6 +1621,14 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     return fail(TF_ERR_CUDA);
   }
   r->ctrl_stream = s;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&r->ctl_host_dev, r->ctl_host, 0) != cudaSuccess) {
+    tf_set_error("snapshot stream / mapping failed");
+    return fail(TF_ERR_CUDA);
+  }
+  r->snap_stream = s;
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TF_ERR_CUDA);
   *out = r;
   return TF_OK;
@@ -1619,6 +1639,7 @@ extern "C" int tf_ring_destroy(tf_ring* r) {
   cudaSetDevice(r->device);
   cudaDeviceSynchronize();
   if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
+  if (r->snap_stream) cudaStreamDestroy((cudaStream_t)r->snap_stream);
   cudaFree(r->payload);
   cudaFree(r->ctl);
   cudaFree(r->dcons);

@@ -87,7 +87,9 @@ struct tf_ring {
   uint8_t* meta = nullptr;        // host pinned mapped (device alias == same VA)
   DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
-  DevCtl* ctl_host = nullptr;     // pinned snapshot target
+  DevCtl* ctl_host = nullptr;     // pinned, host-mapped snapshot target
+  DevCtl* ctl_host_dev = nullptr; // its device alias (snapshot kernel)
+  void* snap_stream = nullptr;    // high-priority stream of the snapshot kernel
   void* ctrl_stream = nullptr;    // cudaStream_t for consumer-cursor updates
   // consumer-role state (host)
   std::mutex mu;

@@ -282,7 +282,8 @@ class ExportPipeline:
             self._st, batch.batch_id, addr, len(dst)))
         view = memoryview(dst)
         for desc, start in batch.entries:
-            out.items.append((desc, view[start:start + desc.payload_len]))
+            out.items.append((desc, view[start:start + desc.payload_len],
+                              addr + start if addr else None))
         self.pageable_bytes_in_flight += batch.bytes_total
         self._note_transient()
         self.events.append(DrainEvent(now, "staged", batch.reason,
@@ -301,9 +302,45 @@ class ExportPipeline:
         meta = self.fifo.match(desc, self._hook_name_of(desc.hook_id))
         return split_payload(meta, payload, copy=self.copy_payloads)
 
+    def _sink_captures(self, batch: PageableBatch, sink, now: float) -> int:
+        """Fast path for sinks with ``write_captures``: match every payload
+        to its FIFO entry (MetaMismatch stays fatal) and hand the whole
+        batch over at once; no per-record Python objects. Returns bytes."""
+        caps = []
+        total = recs = 0
+        for item in batch.items:
+            desc, payload = item[0], item[1]
+            addr = item[2] if len(item) > 2 else None
+            meta = self.fifo.match(desc, self._hook_name_of(desc.hook_id))
+            n = len(payload)
+            if n != meta.expected_payload_len:  # split_payload's check
+                raise MetaMismatch(
+                    f"payload {n} bytes != expected {meta.expected_payload_len}")
+            caps.append((meta, payload, addr))
+            total += n
+            recs += len(meta.request_ids)
+        try:
+            sink.write_captures(caps)
+        except Exception as exc:  # sink faults are isolated (exporter.py:266-271)
+            self.sink_failures += 1
+            self.events.append(DrainEvent(now, "sink-error", str(exc), recs, total))
+        else:
+            self.records_out += recs
+            self.bytes_out += total
+        self.pageable_bytes_in_flight -= total
+        return total
+
     def sink_batch(self, batch: PageableBatch, sink, now: float = 0.0) -> None:
         total = 0
-        for desc, payload in batch.items:
+        if getattr(sink, "write_captures", None) is not None:
+            total = self._sink_captures(batch, sink, now)
+            self.batches_sunk += 1
+            self.events.append(DrainEvent(now, "sunk", batch.reason,
+                                          len(batch.items), total))
+            if batch._release is not None:
+                batch._release()
+            return
+        for desc, payload, *_ in batch.items:
             n = len(payload)
             total += n
             records = self.reconstruct(desc, payload)
@@ -388,7 +425,7 @@ class ExportPipeline:
         for i in range(n):
             d = Descriptor.from_c(pb.descs[i])
             s = pb.starts[i]
-            batch.items.append((d, view[s:s + d.payload_len]))
+            batch.items.append((d, view[s:s + d.payload_len], pb.payload + s))
         with self._lock:
             self.pageable_bytes_in_flight += pb.bytes_total
             self.sink_batch(batch, self._sink, time.monotonic())

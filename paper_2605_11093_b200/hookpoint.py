@@ -75,7 +75,8 @@ class Observer:
                  max_tokens: int = 8192, max_rows_sampled: int = 1 << 22,
                  sampler: TokenSampler | None = None,
                  sampled_hooks: frozenset = frozenset(),
-                 rank_coords: tuple = (0, 0), wait_timeout: float = 60.0):
+                 rank_coords: tuple = (0, 0), wait_timeout: float = 60.0,
+                 flat_rows: int = 0, persistent: bool = False):
         t = torch()
         self.registry = registry
         self.policy = policy or PolicyConfig()
@@ -90,7 +91,9 @@ class Observer:
         self.sampled_hooks = frozenset(sampled_hooks)
         self.rank_coords = rank_coords
         dev = f"cuda:{self.device}"
-        self.keep_req = t.ones(max_batch, dtype=t.uint8, device=dev)
+        # a persistent observer keeps nothing until its first begin_step
+        self.keep_req = (t.zeros if persistent else t.ones)(max_batch, dtype=t.uint8,
+                                                            device=dev)
         # per-token keep for sampled hooks, expanded over each hook's row
         # groups: a (heads, tokens, tokens) attention map has `heads` query
         # rows per token; fixed buffers so CUDA-graph replays see updates
@@ -102,8 +105,21 @@ class Observer:
             self._keep_m[m] = t.zeros(max(1, n), dtype=t.uint8, device=dev)
         self.keep_tok = self._keep_m.get(1)
         self._flat = {}
-        self._flat_rows = max_batch * 64
+        self._flat_rows = max(flat_rows, max_batch * 64)
+        # serving engines record HookPoints into their CUDA graphs once, so
+        # captures stay armed between steps (persistent=True) and the keep
+        # buffers are allocated up front at their final size (flat_rows):
+        # a replay reads whatever keep vector the last begin_step uploaded
+        self.persistent = persistent
+        self._pinned = {}
         self._layout = "batch"
+        if flat_rows:
+            self._flat_buf("req", flat_rows)
+            if self.sampled_hooks:
+                self._flat_buf("tok", flat_rows)
+            # engines that run (tokens, ...) activations: forwards before the
+            # first begin_step (profiling, graph capture) see all-zero keeps
+            self._layout = "flat"
         self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
         self.token = t.zeros(1, dtype=t.uint8, device=dev)  # custom-op ordering token
         self.index = _register_observer(self)
@@ -112,7 +128,9 @@ class Observer:
         self._plan: StepPlan | None = None
         self._batch = []
         self._tok_sel: dict[int, list[int]] = {}
-        self.active = False
+        # persistent: armed from the start, so HookPoints are recorded into
+        # CUDA graphs captured before the first step (keep vector all zero)
+        self.active = persistent
         self.launches = 0
         self.steps = 0
 
@@ -139,13 +157,15 @@ class Observer:
     # -- per step --------------------------------------------------------------
 
     def begin_step(self, batch, step_seq: int, stream=None,
-                   layout: str = "batch") -> StepPlan:
+                   layout: str = "batch", rows_total: int | None = None) -> StepPlan:
         """Plan the step, honour the flush gate, queue metadata, upload keep.
 
         ``layout="batch"``: activations are (B, T, ...) with uniform T
         (the reference's model). ``layout="flat"``: continuous batching —
         activations are (sum of tokens, ...) in batch order and requests may
-        carry different token counts (prefill chunks beside decodes).
+        carry different token counts (prefill chunks beside decodes);
+        ``rows_total`` is the padded row count the engine runs (CUDA-graph
+        batch sizes), whose padding rows are never kept.
         """
         t = torch()
         batch = list(batch)
@@ -176,23 +196,36 @@ class Observer:
         self.fifo.extend(metas)
         s = stream if stream is not None else t.cuda.current_stream(self.device)
         with t.cuda.stream(s):
-            step = t.tensor([step_seq & 0x7FFFFFFF], dtype=t.int32).pin_memory()
+            busy = self._pinned.get("_busy")
+            if busy is not None:  # the previous step's uploads have left
+                busy.synchronize()
+            step = self._pinned.get("step")
+            if step is None:
+                step = t.zeros(1, dtype=t.int32).pin_memory()
+                self._pinned["step"] = step
+            step[0] = step_seq & 0x7FFFFFFF
             self.step_buf.copy_(step, non_blocking=True)
             if flat:
-                # per-row keep over the flat token layout
-                rows = sum(r.tokens for r in batch)
-                flags = t.zeros(max(1, rows), dtype=t.uint8)
-                samp = t.zeros(max(1, rows), dtype=t.uint8)
-                pos = 0
-                for r in batch:
-                    if r.request_id in kept_set:
-                        flags[pos:pos + r.tokens] = 1
+                # per-row keep over the flat token layout (padding rows 0)
+                rows = max(sum(r.tokens for r in batch), rows_total or 0)
+                flags = self._host_rows("req", max(1, rows))
+                samp = self._host_rows("tok", max(1, rows)) if sel else None
+                import numpy as np
+                ntok = np.fromiter((r.tokens for r in batch), dtype=np.int64,
+                                   count=len(batch))
+                kmask = np.fromiter((r.request_id in kept_set for r in batch),
+                                    dtype=np.uint8, count=len(batch))
+                fl = np.repeat(kmask, ntok)
+                flags.numpy()[:fl.size] = fl
+                if sel:
+                    pos = 0
+                    for r in batch:
                         for tok in sel.get(r.request_id, ()):
                             samp[pos + tok] = 1
-                    pos += r.tokens
-                self._upload(self._flat_buf("req", rows), flags)
+                        pos += r.tokens
+                self._upload_pinned(self._flat_buf("req", rows), flags)
                 if sel:
-                    self._upload(self._flat_buf("tok", rows), samp)
+                    self._upload_pinned(self._flat_buf("tok", rows), samp)
             else:
                 keep = t.tensor(list(plan.keep) or [0], dtype=t.uint8)
                 self._upload(self.keep_req, keep)
@@ -204,11 +237,38 @@ class Observer:
                             flags[i, 0, tok] = 1
                     for m, buf in self._keep_m.items():
                         self._upload(buf, flags.expand(len(batch), m, tokens).reshape(-1))
+            ev = self._pinned.get("_ev")
+            if ev is None:
+                ev = t.cuda.Event()
+                self._pinned["_ev"] = ev
+            ev.record(s)
+            self._pinned["_busy"] = ev
         self._plan, self._batch, self._tok_sel = plan, batch, sel
         self._layout = layout
-        self.active = bool(plan.kept_ids)
+        self.active = bool(plan.kept_ids) or self.persistent
         self.steps += 1
         return plan
+
+    def _host_rows(self, kind: str, rows: int):
+        """Zeroed view of a reusable pinned host buffer (flat keep flags);
+        begin_step waits for the previous upload from it before reuse."""
+        t = torch()
+        busy = self._pinned.get("_busy")
+        if busy is not None:  # the previous step's upload has left the buffer
+            busy.synchronize()
+        buf = self._pinned.get(kind)
+        if buf is None or buf.numel() < rows:
+            buf = t.zeros(max(rows, self._flat_rows), dtype=t.uint8).pin_memory()
+            self._pinned[kind] = buf
+        v = buf[:rows]
+        v.zero_()
+        return v
+
+    @staticmethod
+    def _upload_pinned(dst, src) -> None:
+        if src.numel() > dst.numel():
+            raise ConfigError("keep vector exceeds its device buffer")
+        dst[:src.numel()].copy_(src, non_blocking=True)
 
     @staticmethod
     def _upload(dst, src) -> None:
@@ -229,7 +289,7 @@ class Observer:
 
     def end_step(self, stream=None) -> None:
         self.ring.note_launch(stream)
-        self.active = False
+        self.active = self.persistent
 
     def graph_capture(self):
         """Context manager for recording a CUDA graph of one step: enabled

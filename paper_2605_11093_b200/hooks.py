@@ -158,6 +158,7 @@ class HookRegistry:
             self._ids[h.name] = i
         self._enabled = frozenset(range(len(self.hooks)))
         self._staged: frozenset | None = None
+        self._plan_cache: dict = {}
 
     def __len__(self) -> int:
         return len(self.hooks)
@@ -189,6 +190,25 @@ class HookRegistry:
 
     def slice_bytes(self, hook_id: int, tokens: int) -> int:
         return self.hooks[hook_id].slice_bytes(tokens, self.hidden_extent)
+
+    def plan_entries(self, tokens: int) -> tuple:
+        """(hook_id, hook) and resolved per-request shape of every enabled
+        hook in firing order for a step of ``tokens`` tokens; cached per
+        enabled set and token count (the planner asks every step)."""
+        c = self._plan_cache
+        if c.get(None) is not self._enabled:
+            c.clear()
+            c[None] = self._enabled
+        e = c.get(tokens)
+        if e is None:
+            e = tuple((hid, self.hooks[hid],
+                       self.hooks[hid].resolve_shape(tokens, self.hidden_extent))
+                      for hid in sorted(self._enabled))
+            if len(c) > 512:
+                c.clear()
+                c[None] = self._enabled
+            c[tokens] = e
+        return e
 
 
 def install_hooks(model: ModelSpec, specs: list[HookSpec],

@@ -1,0 +1,35 @@
+"""vLLM 0.22 integration (BASELINE configs[3]) on a tiny
+random-init Llama, each mode in its own process (scripts/vllm_check.py):
+eager mode is bit-exact against torch hooks at the same sites; CUDA-graph
+mode (the serving configuration) delivers exactly one record per step,
+hook and scheduled request with the scheduled row count."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(mode):
+    pytest.importorskip("vllm")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "vllm_check.py"),
+                          "--mode", mode], capture_output=True, text=True, timeout=1200,
+                         cwd=ROOT)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert res.returncode == 0 and lines, res.stderr[-3000:]
+    return json.loads(lines[-1])
+
+
+def test_vllm_eager_records_bit_exact():
+    out = _run("eager")
+    assert out["ok"], out
+
+
+def test_vllm_cuda_graph_records_complete():
+    out = _run("graph")
+    assert out["ok"], out
