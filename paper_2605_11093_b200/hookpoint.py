@@ -30,6 +30,7 @@ observer's ``TokenSampler``; its records carry ``row_counts`` and
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 
 from . import _native as N
@@ -37,7 +38,7 @@ from ._device import torch
 from .errors import ConfigError, PolicyUnderestimate
 from .exporter import DrainConfig, ExportPipeline
 from .hooks import HookRegistry, RowSource, capture_args, launch_capture
-from .policy import PolicyConfig, StepPlan, prepare_step
+from .policy import COMPLETENESS, PolicyConfig, StepPlan, prepare_step
 from .records import TensorMeta, TensorMetaFIFO
 from .rings import RingConfig, RingPair
 
@@ -123,6 +124,7 @@ class Observer:
         self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
         self.token = t.zeros(1, dtype=t.uint8, device=dev)  # custom-op ordering token
         self.index = _register_observer(self)
+        self._sc = (None, 0.0, 0, 0)  # policy snapshot, time, bytes planned since, max capture
         self.max_batch = max_batch
         self._names = {h.name: i for i, h in enumerate(registry.hooks)}
         self._plan: StepPlan | None = None
@@ -175,9 +177,20 @@ class Observer:
             raise ConfigError(f"unknown activation layout {layout!r}")
         flat = layout == "flat"
         self.registry.commit_filter()
-        plan = prepare_step(self.policy, batch, self.ring, self.registry,
-                            step_seq=step_seq, rank_coords=self.rank_coords,
-                            ragged=flat)
+        if not batch:  # engine warm-up / dummy forwards: nothing to keep
+            plan = StepPlan(keep=(), flush_before=False, fifo_entries=(), kept_ids=(),
+                            dropped_ids=(), free_bytes_at_plan=0)
+        else:
+            plan = prepare_step(self.policy, batch, self._policy_ring(), self.registry,
+                                step_seq=step_seq, rank_coords=self.rank_coords,
+                                ragged=flat)
+            if self.policy.mode == COMPLETENESS:
+                st, t0, since, big = self._sc
+                for m in plan.fifo_entries:
+                    n = m.expected_payload_len
+                    since += n + 16
+                    big = max(big, n)
+                self._sc = (st, t0, since, big)
         if plan.flush_before:
             self.flush()
         metas = list(plan.fifo_entries)
@@ -269,6 +282,30 @@ class Observer:
         if src.numel() > dst.numel():
             raise ConfigError("keep vector exceeds its device buffer")
         dst[:src.numel()].copy_(src, non_blocking=True)
+
+    def _policy_ring(self):
+        """The ring as the planner sees it. Completeness only needs to know
+        whether occupancy crossed the flush watermark, and occupancy cannot
+        grow faster than the bytes this host has planned since the last
+        device snapshot, so that snapshot is reused while snapshot +
+        planned bytes + slack (dead-skip waste) stays under the watermark:
+        the decision is the one a fresh snapshot would give, without a
+        device round trip per step. Best-effort replays the allocator
+        (would_fit) and always reads the device."""
+        if self.policy.mode != COMPLETENESS:
+            return self.ring
+        return _CompletenessRingView(self)
+
+    def _snapshot_for_policy(self):
+        st, t0, since, big = self._sc
+        now = time.monotonic()
+        if st is not None and now - t0 < 0.5:
+            bound = st.occupancy + since + 2 * big + (1 << 16)
+            if bound < self.policy.pressure_watermark * st.payload_capacity:
+                return st
+        st = self.ring.state()
+        self._sc = (st, now, 0, big)
+        return st
 
     @staticmethod
     def _upload(dst, src) -> None:
@@ -363,6 +400,20 @@ class Observer:
             full=self.policy.full_mode)
         launch_capture(self.ring, args, stream)
         self.launches += 1
+
+
+class _CompletenessRingView:
+    """RingPair proxy whose state() may return a recent snapshot (see
+    Observer._policy_ring); everything else goes to the ring."""
+
+    def __init__(self, obs: "Observer") -> None:
+        self._obs = obs
+
+    def state(self):
+        return self._obs._snapshot_for_policy()
+
+    def __getattr__(self, name):
+        return getattr(self._obs.ring, name)
 
 
 def _row_groups(hook, hidden: int) -> int:

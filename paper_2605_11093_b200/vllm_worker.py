@@ -198,7 +198,8 @@ class ObservedWorker(Worker):
                               page_out="handoff"),
             policy=policy, sink=self._tf_sink, device=self.local_rank,
             max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True)
-        obs.exporter.copy_payloads = False
+        # records that outlive the batch (ListSink) must own their bytes
+        obs.exporter.copy_payloads = cfg.get("sink") == "list"
         obs.start()
         self._tf_obs = obs
         self._tf_handles = attach_vllm_llama(model, obs, sites)

@@ -27,9 +27,9 @@ def _run(mode):
 
 def test_vllm_eager_records_bit_exact():
     out = _run("eager")
-    assert out["ok"], out
+    assert out["ok"], json.dumps(out)
 
 
 def test_vllm_cuda_graph_records_complete():
     out = _run("graph")
-    assert out["ok"], out
+    assert out["ok"], json.dumps(out)
