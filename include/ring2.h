@@ -76,6 +76,10 @@ typedef struct tf_descriptor {
 #define TF_DESC_DEAD_SKIP 0x1u     /* skip_before bytes are a dead region */
 #define TF_DESC_EMPTY_RESET 0x2u   /* skip_before bytes were an empty-ring reset */
 #define TF_DESC_HOST_RESERVED 0x4u /* region registered via tf_ring_reserve */
+/* Bits 16..31 of flags (device-internal, cleared before descriptors are
+ * handed out): the number of capture CTAs whose completion flags the host
+ * must see before it may take the slot (0: posted after completion). */
+#define TF_DESC_CTA_SHIFT 16u
 
 typedef struct tf_ring_config {
   uint64_t payload_capacity; /* bytes, >0, multiple of 16 (rings.py:75-81) */

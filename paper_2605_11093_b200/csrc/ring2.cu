@@ -296,6 +296,7 @@ struct CapParams {
   const DevConsumer* dcons;
   DevCtl* ctl;
   uint64_t timeout_ns;
+  uint8_t* done_flags;        // mapped host memory, kMaxFlagCtas per slot
 };
 
 enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
@@ -317,6 +318,8 @@ struct CapShared {
   uint64_t fast_skip, fast_mh, fast_seq;
   tf_pstate fast_p;
   uint64_t old_L, old_L_phys, old_head;  // snapshot inputs of the fast plan
+  uint64_t slot_idx;                      // meta slot of a published capture
+  uint32_t flagmode;                      // completion via per-CTA flags
   SnapVals next;                          // last CTA: the next snapshot
   uint64_t desc[8];
   uint64_t* slot;
@@ -537,14 +540,12 @@ __device__ __forceinline__ bool fast_plan(const CapParams& P, const SnapRegs& r,
   return true;
 }
 
-// Last CTA of a fast-path launch, thread 0: the descriptor, the result
-// record and the canonical state, all stores. Its inputs were loaded before
-// the done count (step number, consumer cursors), so nothing here waits on
-// memory.
-__device__ void fast_finish(const CapParams& P, CapShared& sh, uint64_t bytes, uint64_t rows,
-                            uint32_t step, uint64_t L, uint64_t mt, uint64_t k0) {
-  DevCtl* c = P.ctl;
-  const uint64_t len = tf_round_up16(bytes), seq = sh.fast_seq;
+// Fast path, thread 0 of the publishing CTA: the 64-B descriptor of this
+// capture. With completion flags (n_ctas > 0) it is posted as soon as the
+// plan is known; the host takes the slot only when all n_ctas CTAs have set
+// their completion byte.
+__device__ void fast_desc(const CapParams& P, CapShared& sh, uint64_t bytes, uint64_t rows,
+                          uint32_t step, uint32_t n_ctas) {
   tf_descriptor d;
   d.payload_offset = sh.off;
   d.payload_len = bytes;
@@ -552,28 +553,38 @@ __device__ void fast_finish(const CapParams& P, CapShared& sh, uint64_t bytes, u
   d.step_seq = step;
   d.ready_seq = TF_READY_SENTINEL;
   d.skip_before = sh.fast_skip;
-  d.flags = sh.fast_kind;
+  d.flags = sh.fast_kind | (n_ctas << TF_DESC_CTA_SHIFT);
   d.n_rows = (uint32_t)rows;
-  d.capture_seq = seq;
+  d.capture_seq = sh.fast_seq;
   d.checksum = 0;
   uint64_t mh = sh.fast_mh;
   sh.publish = 0;
   if (!(P.flags & TF_CAP_DEFER_PUBLISH)) {
     d.ready_seq = mh;
     d.checksum = tf_desc_checksum(reinterpret_cast<const uint64_t*>(&d));
-    sh.slot = reinterpret_cast<uint64_t*>(P.meta + umod64(mh, P.slots) * TF_DESCRIPTOR_SIZE);
+    sh.slot_idx = umod64(mh, P.slots);
+    sh.slot = reinterpret_cast<uint64_t*>(P.meta + sh.slot_idx * TF_DESCRIPTOR_SIZE);
     sh.publish = 1;
     mh += 1;
   }
   const uint64_t* w = reinterpret_cast<const uint64_t*>(&d);
   for (int i = 0; i < 8; ++i) sh.desc[i] = w[i];
-  // next snapshot, derived incrementally (skip + len <= cap and
-  // L - old_L <= cap, so one conditional subtraction replaces each modulo)
+  sh.next.mh = mh;
+}
+
+// Fast path, thread 0 of the committing CTA, after the capture's copy: the
+// result record, the canonical state and the next snapshot (derived
+// incrementally: skip + len <= cap and L - old_L <= cap, so one conditional
+// subtraction replaces each 64-bit modulo).
+__device__ void fast_state(const CapParams& P, CapShared& sh, uint64_t bytes, uint64_t rows,
+                           uint64_t L, uint64_t mt, uint64_t k0) {
+  DevCtl* c = P.ctl;
+  const uint64_t len = tf_round_up16(bytes), seq = sh.fast_seq;
+  const uint64_t mh = sh.next.mh;
   {
     const uint64_t cap = P.cap;
     SnapVals& v = sh.next;
     v.p = sh.fast_p;
-    v.mh = mh;
     v.cseq = seq;
     v.mt = mt;
     if (L < sh.old_L) L = sh.old_L;
@@ -609,8 +620,10 @@ __device__ void fast_finish(const CapParams& P, CapShared& sh, uint64_t bytes, u
   r.payload_offset = sh.off;
   r.payload_len = bytes;
   r.skip_before = sh.fast_skip;
-  r.ready_seq = d.ready_seq;
-  r.desc = d;
+  const tf_descriptor* d = reinterpret_cast<const tf_descriptor*>(sh.desc);
+  r.ready_seq = d->ready_seq;
+  r.desc = *d;
+  r.desc.flags &= (1u << TF_DESC_CTA_SHIFT) - 1u;
   atomicAdd((unsigned long long*)&c->captures, 1ull);
   atomicAdd((unsigned long long*)&c->bytes_reserved, (unsigned long long)len);
   if (sh.fast_kind & TF_DESC_DEAD_SKIP)
@@ -618,6 +631,16 @@ __device__ void fast_finish(const CapParams& P, CapShared& sh, uint64_t bytes, u
   const uint64_t dt = globaltimer() - k0;
   c->last_kernel_ns = dt;
   atomicAdd((unsigned long long*)&c->kernel_ns, (unsigned long long)dt);
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_u8(uint8_t* p, uint8_t v) {
+  asm volatile("st.relaxed.sys.global.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void red_add_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Non-leader CTAs wait for the leader's plan with exponential backoff: under
@@ -813,7 +836,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     TSTAMP(t_fast);
     if (fast) {
       sh.status = TF_OK;
+      // completion flags: every CTA reports; CTA 0 posts the descriptor now
+      sh.flagmode = gridDim.x <= kMaxFlagCtas && P.done_flags != nullptr;
+      if (sh.flagmode) red_add_gpu(&P.ctl->readers, 1u);  // snapshot consumed
+      if (blockIdx.x == 0 || !sh.flagmode)
+        fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? gridDim.x : 0u);
     } else {
+      sh.flagmode = 0;
       uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
       leader = (t == 0);
       if (leader) {
@@ -859,6 +888,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
   __syncthreads();
   TSTAMP(t_table);
+  if (sh.flagmode && blockIdx.x == 0 && sh.publish && warp == 0 && lane < 8)
+    sh.slot[lane] = sh.desc[lane];  // early post; the host waits for the flags
   // Work order. With a global rank table (small keep, or no keep) the warps
   // of all CTAs walk the segments grid-interleaved, so at any moment the
   // active reads and writes cover one contiguous window of the source and
@@ -1024,9 +1055,56 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     }
   }
 
-  // ---- 4. the last CTA to retire publishes ----
+  // ---- 4. completion ----
   if (TF_ABL & 2) return;
   __syncthreads();
+  if (sh.flagmode) {
+    // Fast path: each CTA makes its payload stores visible system-wide and
+    // sets its completion byte (the host takes the descriptor CTA 0 posted
+    // once every byte is set); CTA 0 then commits the state and the next
+    // snapshot once every CTA has read the current one. No last-CTA
+    // election, no round trip on the kernel's critical path.
+    if (tid == 0) {
+      if (sh.publish) {
+        fence_acq_rel_sys();
+        st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + blockIdx.x, 1);
+      }
+      if (blockIdx.x == 0) {
+        const uint64_t L_now = ld_relaxed_gpu(&P.dcons->L);
+        const uint64_t mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
+        uint32_t ns = 32;
+        while (ld_acquire_gpu(&P.ctl->readers) < gridDim.x) {
+          __nanosleep(ns);
+          ns = ns < 256 ? ns * 2 : ns;
+        }
+        fast_state(P, sh, out_bytes, n_rows, L_now, mt_now, t_entry);
+        P.ctl->readers = 0;  // re-armed for the next launch (kernel boundary)
+      }
+    }
+    if (blockIdx.x == 0) {
+      __syncthreads();
+      if (warp == 1) write_snap(P.ctl, sh.next, lane, 32);  // next launch's snapshot
+#ifdef TF_TRACE
+      if (tid == 0) {
+        const int slot = int(sh.fast_seq % kTrLaunches);
+        g_pub[slot][0] = globaltimer();
+        g_pub[slot][1] = gridDim.x;
+      }
+#endif
+    }
+#ifdef TF_TRACE
+    if (tid == 0 && blockIdx.x < kTrCtas) {
+      const int slot = int(sh.fast_seq % kTrLaunches);
+      g_stamp[slot][blockIdx.x][0] = t_entry;
+      g_stamp[slot][blockIdx.x][1] = t_plan;
+      g_stamp[slot][blockIdx.x][2] = globaltimer();
+      g_stamp[slot][blockIdx.x][3] = t_scan;
+      g_stamp[slot][blockIdx.x][4] = t_fast;
+      g_stamp[slot][blockIdx.x][5] = t_table;
+    }
+#endif
+    return;
+  }
   uint64_t L_now = 0, mt_now = 0;
   if (tid == 0) {
     // consumer cursors for the next snapshot, loaded while the fence and the
@@ -1055,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   if (sh.is_last) {
     if (tid == 0) {
       if (sh.fast) {
-        if (!(TF_ABL & 32)) fast_finish(P, sh, out_bytes, n_rows, step, L_now, mt_now, t_entry);
+        if (!(TF_ABL & 32)) fast_state(P, sh, out_bytes, n_rows, L_now, mt_now, t_entry);
       } else {
         last_cta_prepare(P, sh);
         write_snap_ctl(P);
@@ -1531,6 +1609,7 @@ static CapParams base_params(tf_ring* r) {
   P.meta = r->meta;
   P.dcons = r->dcons;
   P.ctl = r->ctl;
+  P.done_flags = r->done_flags;
   P.timeout_ns = r->cfg.wait_timeout_ns ? r->cfg.wait_timeout_ns : 30000000000ull;
   return P;
 }
@@ -1579,6 +1658,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     if (r->ctl) cudaFree(r->ctl);
     if (r->dcons) cudaFree(r->dcons);
     if (r->meta) cudaFreeHost(r->meta);
+    if (r->done_flags) cudaFreeHost(r->done_flags);
     if (r->ctl_host) cudaFreeHost(r->ctl_host);
     if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
     delete r;
@@ -1593,11 +1673,14 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
   }
   size_t meta_bytes = size_t(cfg->meta_slots) * TF_DESCRIPTOR_SIZE;
   if (cudaHostAlloc((void**)&r->meta, meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->done_flags, size_t(cfg->meta_slots) * kMaxFlagCtas,
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
       cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
     tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_ALLOCATION);
   }
   memset(r->meta, 0, meta_bytes);
+  memset(r->done_flags, 0, size_t(cfg->meta_slots) * kMaxFlagCtas);
   for (uint32_t s = 0; s < cfg->meta_slots; ++s)  // rings.py:213-215
     reinterpret_cast<uint64_t*>(r->meta + size_t(s) * TF_DESCRIPTOR_SIZE)[3] = TF_READY_SENTINEL;
   if (cudaMalloc(&r->ctl, sizeof(DevCtl)) != cudaSuccess ||
@@ -1644,6 +1727,7 @@ extern "C" int tf_ring_destroy(tf_ring* r) {
   cudaFree(r->ctl);
   cudaFree(r->dcons);
   cudaFreeHost(r->meta);
+  cudaFreeHost(r->done_flags);
   cudaFreeHost(r->ctl_host);
   delete r;
   return TF_OK;
@@ -2063,6 +2147,21 @@ static bool slot_verified(const uint8_t* raw, tf_descriptor* d) {
   return true;
 }
 
+// A posted slot is complete when its checksum verifies and, for a capture
+// posted before its copy finished, every CTA has set its completion byte.
+// The CTA count is stripped from the flags handed out.
+static bool slot_complete(const tf_ring* r, uint64_t slot, tf_descriptor* d) {
+  if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, d)) return false;
+  const uint32_t n = d->flags >> TF_DESC_CTA_SHIFT;
+  if (n) {
+    const uint8_t* f = r->done_flags + slot * kMaxFlagCtas;
+    for (uint32_t i = 0; i < n; ++i)
+      if (__atomic_load_n(f + i, __ATOMIC_ACQUIRE) != 1) return false;
+  }
+  d->flags &= (1u << TF_DESC_CTA_SHIFT) - 1u;
+  return true;
+}
+
 int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
                      uint32_t* n, bool consume) {
   uint32_t got = 0;
@@ -2074,8 +2173,9 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
     uint64_t ready = slot_ready(r, slot);
     if (ready == TF_READY_SENTINEL) break;
     tf_descriptor d;
-    // words may still be landing: accept only a slot whose checksum verifies
-    if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, &d)) break;
+    // words may still be landing: accept only a slot whose checksum
+    // verifies (and whose capture CTAs have all reported)
+    if (!slot_complete(r, slot, &d)) break;
     if (consume) {
       if (d.ready_seq != r->consumed) {  // rings.py:397-401
         tf_set_error("descriptor sequence %llu out of order, expected %llu",
@@ -2083,6 +2183,9 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
         *n = got;
         return TF_ERR_PROTOCOL;
       }
+      const uint32_t n_ctas = reinterpret_cast<const tf_descriptor*>(
+          r->meta + slot * TF_DESCRIPTOR_SIZE)->flags >> TF_DESC_CTA_SHIFT;
+      if (n_ctas) memset(r->done_flags + slot * kMaxFlagCtas, 0, n_ctas);
       uint64_t* rp = reinterpret_cast<uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE) + 3;
       __atomic_store_n(rp, TF_READY_SENTINEL, __ATOMIC_RELEASE);
       r->meta_tail = ++tail;
@@ -2124,8 +2227,7 @@ extern "C" int tf_ring_ready_bytes(tf_ring* r, uint64_t* n) {
   for (uint64_t i = 0; i < slots; ++i) {
     uint64_t slot = (r->meta_tail + i) % slots;
     tf_descriptor d;
-    if (slot_ready(r, slot) == TF_READY_SENTINEL ||
-        !slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, &d))
+    if (slot_ready(r, slot) == TF_READY_SENTINEL || !slot_complete(r, slot, &d))
       break;
     total += d.payload_len;
   }

@@ -49,6 +49,7 @@ struct alignas(128) ProdSnap {
   uint64_t used, head, tail, pad1[5];
 };
 constexpr int kSnapReplicas = 8;
+constexpr int kMaxFlagCtas = 512;   // completion bytes per meta slot
 
 struct alignas(128) DevCtl {
   // allocator (producer role)
@@ -60,6 +61,7 @@ struct alignas(128) DevCtl {
   // per-launch handshake between the CTAs of one capture kernel; launches
   // on one producer stream are serialised, the last CTA re-arms these.
   uint32_t arrive, done, plan_flag, plan_status;
+  uint32_t readers, pad_r;  // fast-path CTAs that have read the snapshot (this launch)
   uint64_t plan_off, plan_skip, plan_len, plan_bytes, plan_rows, plan_seq;
   uint32_t plan_kind, pad0;
 
@@ -85,6 +87,10 @@ struct tf_ring {
   tf_ring_config cfg{};
   uint8_t* payload = nullptr;     // device
   uint8_t* meta = nullptr;        // host pinned mapped (device alias == same VA)
+  // per meta slot, one completion byte per capture CTA (host pinned mapped):
+  // fast-path captures post their descriptor early and every CTA sets its
+  // byte after its payload stores; the host takes the slot once all are set
+  uint8_t* done_flags = nullptr;
   DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
   DevCtl* ctl_host = nullptr;     // pinned, host-mapped snapshot target

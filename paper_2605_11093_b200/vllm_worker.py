@@ -252,7 +252,7 @@ class ObservedWorker(Worker):
                 batch.append(StepRequest(ent[0], ent[1], "", int(n), start))
         # dummy / warm-up forwards get an empty batch: every row dropped
         obs.begin_step(batch, self._tf_step, layout="flat", rows_total=rows_total)
-        if self._tf_cfg.get("debug_clone"):
+        if self._tf_cfg.get("debug_clone") or self._tf_cfg.get("sink") == "list":
             self._tf_layouts[self._tf_step] = [(r.request_id, r.tokens) for r in batch]
         self._tf_step += 1
         self._tf_steps += 1

@@ -20,6 +20,7 @@ from paper_2605_11093_b200.hooks import RowSource, capture_args, launch_capture 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=16)
 ap.add_argument("--sizes-mib", default="1,4,16,32,64,112,224")
+ap.add_argument("--sizes-kb", default="", help="overrides --sizes-mib (KiB)")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default="gpurun_out/sweep.json")
 args = ap.parse_args()
@@ -66,10 +67,13 @@ def timed_graph(fn, reps):
     return statistics.median(out)
 
 
-for mib in [int(x) for x in args.sizes_mib.split(",")]:
-    nbytes = mib << 20
+sizes = [int(x) << 10 for x in args.sizes_kb.split(",")] if args.sizes_kb else \
+    [int(x) << 20 for x in args.sizes_mib.split(",")]
+for nbytes in sizes:
+    mib = nbytes / 1048576
     row = nbytes // B
     xs = [torch.empty(nbytes, dtype=torch.uint8, device=dev).random_() for _ in range(min(args.n, 4))]
+    assert nbytes % B == 0
     dsts = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(min(args.n, 4))]
     caps = []
     for i in range(args.n):
