@@ -838,7 +838,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       sh.status = TF_OK;
       // completion flags: every CTA reports; CTA 0 posts the descriptor now
       sh.flagmode = gridDim.x <= kMaxFlagCtas && P.done_flags != nullptr;
-      if (sh.flagmode) red_add_gpu(&P.ctl->readers, 1u);  // snapshot consumed
+      if (sh.flagmode) {
+        red_add_gpu(&P.ctl->readers, 1u);  // snapshot consumed
+        sh.publish = !(P.flags & TF_CAP_DEFER_PUBLISH);  // every CTA reports
+        sh.slot_idx = umod64(sh.fast_mh, P.slots);
+      }
       if (blockIdx.x == 0 || !sh.flagmode)
         fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? gridDim.x : 0u);
     } else {
@@ -1066,7 +1070,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     // election, no round trip on the kernel's critical path.
     if (tid == 0) {
       if (sh.publish) {
+#if TF_FLAG_FENCE_SYS
         fence_acq_rel_sys();
+#else
+        // gpu scope, as the last-CTA publish: the payload is in L2 before
+        // the byte leaves, and the D2H copy engine reads through L2
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
         st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + blockIdx.x, 1);
       }
       if (blockIdx.x == 0) {
@@ -1558,6 +1568,7 @@ __global__ void reserve_kernel(CapParams P, uint64_t len) {
   c->res.payload_offset = off;
   c->res.skip_before = skip;
   c->res.payload_len = len;
+  c->res.capture_seq = c->capture_seq;  // device captures reserved before this one
   write_snap_ctl(P);
 }
 
@@ -2025,7 +2036,7 @@ extern "C" int tf_ring_reserve(tf_ring* r, void* stream, uint64_t length,
   uint64_t off = res.payload_offset, skip = res.skip_before;
   {
     std::lock_guard<std::mutex> g(r->mu);
-    HostRegion hr{off, length, skip, res.n_rows /* kind */};
+    HostRegion hr{off, length, skip, res.n_rows /* kind */, false, true, res.capture_seq};
     r->regions.push_back(hr);
     r->host_reserved[off] = hr;
   }
@@ -2153,9 +2164,13 @@ static bool slot_verified(const uint8_t* raw, tf_descriptor* d) {
 static bool slot_complete(const tf_ring* r, uint64_t slot, tf_descriptor* d) {
   if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, d)) return false;
   const uint32_t n = d->flags >> TF_DESC_CTA_SHIFT;
-  if (n) {
+  if (n) {  // 8 completion bytes per load
     const uint8_t* f = r->done_flags + slot * kMaxFlagCtas;
-    for (uint32_t i = 0; i < n; ++i)
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(f);
+    uint32_t i = 0;
+    for (; i + 8 <= n; i += 8)
+      if (__atomic_load_n(w + i / 8, __ATOMIC_ACQUIRE) != 0x0101010101010101ull) return false;
+    for (; i < n; ++i)
       if (__atomic_load_n(f + i, __ATOMIC_ACQUIRE) != 1) return false;
   }
   d->flags &= (1u << TF_DESC_CTA_SHIFT) - 1u;
@@ -2192,8 +2207,15 @@ int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
       r->consumed += 1;
       advanced = true;
       if (!(d.flags & TF_DESC_HOST_RESERVED)) {
-        r->regions.push_back(HostRegion{d.payload_offset, tf_round_up16(d.payload_len),
-                                        d.skip_before, d.flags, true});
+        // before any host reservation made after this capture was reserved
+        auto it = r->regions.end();
+        while (it != r->regions.begin()) {
+          auto prev = std::prev(it);
+          if (prev->host && !prev->polled && prev->seq >= d.capture_seq) it = prev;
+          else break;
+        }
+        r->regions.insert(it, HostRegion{d.payload_offset, tf_round_up16(d.payload_len),
+                                         d.skip_before, d.flags, true, false, d.capture_seq});
       } else {
         for (HostRegion& h : r->regions)
           if (!h.polled && h.off == d.payload_offset) { h.polled = true; break; }

@@ -80,6 +80,12 @@ struct HostRegion {
   // descriptor polled by the consumer: only a leading run of polled regions
   // may be handed back to the device allocator ahead of its release
   bool polled = false;
+  // reservation order: a device capture's capture_seq, or for a host
+  // reservation the device capture count when it was made (it follows
+  // capture `seq` and precedes capture seq+1); device regions become known
+  // only when polled and are inserted at their reservation position
+  bool host = false;
+  uint64_t seq = 0;
 };
 
 struct tf_ring {

@@ -14,7 +14,7 @@ import zlib
 import pytest
 
 from oracle import workload as W
-from paper_2605_11093_b200 import (BEST_EFFORT, COMPLETENESS, DrainConfig, DType,
+from paper_2605_11093_b200 import (BEST_EFFORT, COMPLETENESS, DROP_RECENT, DrainConfig, DType,
                                    HookSpec, ModelSpec, PolicyConfig, RingConfig,
                                    install_hooks)
 from paper_2605_11093_b200.sinks import FileSink
@@ -120,7 +120,9 @@ def test_verify_without_meta_is_a_config_error(tmp_path):
 def test_gpu_run_verifies(tmp_path, policy, ring):
     spec = WorkloadSpec(5, 16, 6, (3, 0, 2))
     meta = run_synthetic(tmp_path / "run", spec=spec, model=ModelSpec(4, 256), hooks=HOOKS,
-                         seed=2605, ring=ring, policy=PolicyConfig(mode=policy),
+                         seed=2605, ring=ring,
+                         policy=PolicyConfig(mode=policy, strategy=DROP_RECENT)
+                         if policy == BEST_EFFORT else PolicyConfig(mode=policy),
                          drain=DrainConfig(min_ready_entries=1, staging_buffer_size=1 << 20))
     ok, rep = verify_dataset(tmp_path / "run")
     assert ok, rep
