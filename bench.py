@@ -183,6 +183,37 @@ def committed_traffic():
 # ---------------------------------------------------------------------------
 # leg: value (device-resident inputs)
 # ---------------------------------------------------------------------------
+def measure_bidir(dev, nbytes=256 << 20, reps=5):
+    """Pinned H2D and D2H copies of `nbytes` running at the same time on two
+    streams (the e2e leg's traffic pattern): GB/s per direction, best of
+    `reps`. The e2e number is bounded by these, not by the one-way peak."""
+    import torch
+    h_src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_dst = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    best = (0.0, 0.0)
+    for _ in range(reps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(s1):
+            e[0].record(s1)
+            d_a.copy_(h_src, non_blocking=True)
+            e[1].record(s1)
+        with torch.cuda.stream(s2):
+            e[2].record(s2)
+            h_dst.copy_(d_b, non_blocking=True)
+            e[3].record(s2)
+        torch.cuda.synchronize(dev)
+        h2d = nbytes / (e[0].elapsed_time(e[1]) * 1e-3) / 1e9
+        d2h = nbytes / (e[2].elapsed_time(e[3]) * 1e-3) / 1e9
+        if h2d + d2h > sum(best):
+            best = (h2d, d2h)
+    return {"h2d_gbs": best[0], "d2h_gbs": best[1],
+            "note": "concurrent pinned H2D + D2H of 256 MiB on two streams, best of 5"}
+
+
 def leg_value(args, dist, dev):
     import torch
 
@@ -685,6 +716,7 @@ def main():
     d2h = __import__("ctypes").c_double()
     N.check(N.lib().tf_measure_d2h(dev.index, 256 << 20, 10, __import__("ctypes").byref(d2h)))
     pcie_peak = d2h.value
+    bidir = measure_bidir(dev)
 
     v = leg_value(args, dist, dev)
     staged, elapsed = dist.reduce([v["staged_bytes"]], "sum")[0], \
@@ -759,6 +791,7 @@ def main():
             "overhead": model,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "pcie_bidirectional": bidir,
             "gpu_launches": v["launches"] * dist.world,
             "clocks": v["clocks"],
             "stall_events": v["stall_events"], "drops": v["drops"],

@@ -713,6 +713,9 @@ template <int MODE, int VW, int IN_DT, int OUT_DT>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams P) {
   __shared__ CapShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // CTA 0 is the controller: it posts the descriptor and commits the
+  // producer state while the others copy; copy CTA cb of cg owns the work.
+  const int cb = int(blockIdx.x) - 1, cg = int(gridDim.x) - 1;
   const int64_t U = P.units;
   const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
 #ifdef TF_TRACE
@@ -753,8 +756,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   if constexpr (MODE == MODE_COPY) {
     if (!(TF_ABL & 256) && (!P.keep || U <= 32)) {
       const int64_t spr0 = (P.words_per_row + kSeg - 1) / kSeg;
-      const int64_t s0 = int64_t(blockIdx.x) * kWarps + warp;
-      if (s0 < U * P.rpu * spr0) {
+      const int64_t s0 = int64_t(cb) * kWarps + warp;
+      if (cb >= 0 && s0 < U * P.rpu * spr0) {
         const int64_t j0 = qdiv(s0, spr0);
         const int64_t k0 = (s0 - j0 * spr0) * kSeg;
         const int64_t k1 = imin64(k0 + kSeg, P.words_per_row);
@@ -837,14 +840,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     if (fast) {
       sh.status = TF_OK;
       // completion flags: every CTA reports; CTA 0 posts the descriptor now
-      sh.flagmode = gridDim.x <= kMaxFlagCtas && P.done_flags != nullptr;
+      sh.flagmode = cg <= kMaxFlagCtas && P.done_flags != nullptr;
       if (sh.flagmode) {
         red_add_gpu(&P.ctl->readers, 1u);  // snapshot consumed
         sh.publish = !(P.flags & TF_CAP_DEFER_PUBLISH);  // every CTA reports
         sh.slot_idx = umod64(sh.fast_mh, P.slots);
       }
       if (blockIdx.x == 0 || !sh.flagmode)
-        fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? gridDim.x : 0u);
+        fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? uint32_t(cg) : 0u);
     } else {
       sh.flagmode = 0;
       uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
@@ -866,8 +869,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     spr = (P.words_per_row + kSeg - 1) / kSeg;
     items = (int64_t)n_rows * spr;
   }
-  const int64_t chunk = qdiv(items + gridDim.x - 1, gridDim.x);
-  const int64_t i0 = imin64(int64_t(blockIdx.x) * chunk, items);
+  const int64_t chunk = qdiv(items + cg - 1, cg);
+  const int64_t i0 = cb < 0 ? items : imin64(int64_t(cb) * chunk, items);
   const int64_t i1 = imin64(i0 + chunk, items);
   const int64_t j_lo = qdiv(i0, spr);
   const int64_t r_lo = qdiv(j_lo, P.rpu);
@@ -900,9 +903,36 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // the ring (DRAM page locality, like a grid-stride copy); otherwise each
   // CTA walks its own contiguous slice [i0, i1) whose ranks its table holds.
   const bool inter = (small || !P.keep) && !(TF_ABL & 64);
-  const int64_t s_first = inter ? int64_t(blockIdx.x) * kWarps + warp : i0 + warp;
-  const int64_t s_step = inter ? int64_t(gridDim.x) * kWarps : kWarps;
   const int64_t s_end = inter ? items : i1;
+  const int64_t s_first = cb < 0 ? s_end : inter ? int64_t(cb) * kWarps + warp : i0 + warp;
+  const int64_t s_step = inter ? int64_t(cg) * kWarps : kWarps;
+
+  // Controller, fast path: commit the allocator state, the result record and
+  // the next snapshot as soon as every CTA has read the current snapshot,
+  // while the copy CTAs copy; then leave (it owns no payload).
+  if (sh.flagmode && cb < 0) {
+    if (tid == 0) {
+      const uint64_t L_now = ld_relaxed_gpu(&P.dcons->L);
+      const uint64_t mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
+      uint32_t ns = 32;
+      while (ld_acquire_gpu(&P.ctl->readers) < gridDim.x) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : ns;
+      }
+      fast_state(P, sh, out_bytes, n_rows, L_now, mt_now, t_entry);
+      P.ctl->readers = 0;  // every CTA has read: re-armed for the next launch
+    }
+    __syncthreads();
+    if (warp == 1) write_snap(P.ctl, sh.next, lane, 32);  // next launch's snapshot
+#ifdef TF_TRACE
+    if (tid == 0) {
+      const int slot = int(sh.fast_seq % kTrLaunches);
+      g_pub[slot][0] = globaltimer();
+      g_pub[slot][1] = gridDim.x;
+    }
+#endif
+    return;
+  }
   auto row_of = [&](int64_t j) -> int64_t {
     int64_t r = qdiv(j, P.rpu);
     int64_t sub = j - r * P.rpu;
@@ -1063,13 +1093,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   if (TF_ABL & 2) return;
   __syncthreads();
   if (sh.flagmode) {
-    // Fast path: each CTA makes its payload stores visible system-wide and
-    // sets its completion byte (the host takes the descriptor CTA 0 posted
-    // once every byte is set); CTA 0 then commits the state and the next
-    // snapshot once every CTA has read the current one. No last-CTA
-    // election, no round trip on the kernel's critical path.
+    // Fast path: each copy CTA orders its payload stores before its
+    // completion byte (the host takes the descriptor the controller posted
+    // once every byte is set). The controller committed the producer state
+    // meanwhile. No last-CTA election, no round trip on the critical path.
     if (tid == 0) {
-      if (sh.publish) {
+      if (sh.publish && cb >= 0) {
 #if TF_FLAG_FENCE_SYS
         fence_acq_rel_sys();
 #else
@@ -1077,30 +1106,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         // the byte leaves, and the D2H copy engine reads through L2
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #endif
-        st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + blockIdx.x, 1);
+        st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + cb, 1);
       }
-      if (blockIdx.x == 0) {
-        const uint64_t L_now = ld_relaxed_gpu(&P.dcons->L);
-        const uint64_t mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
-        uint32_t ns = 32;
-        while (ld_acquire_gpu(&P.ctl->readers) < gridDim.x) {
-          __nanosleep(ns);
-          ns = ns < 256 ? ns * 2 : ns;
-        }
-        fast_state(P, sh, out_bytes, n_rows, L_now, mt_now, t_entry);
-        P.ctl->readers = 0;  // re-armed for the next launch (kernel boundary)
-      }
-    }
-    if (blockIdx.x == 0) {
-      __syncthreads();
-      if (warp == 1) write_snap(P.ctl, sh.next, lane, 32);  // next launch's snapshot
-#ifdef TF_TRACE
-      if (tid == 0) {
-        const int slot = int(sh.fast_seq % kTrLaunches);
-        g_pub[slot][0] = globaltimer();
-        g_pub[slot][1] = gridDim.x;
-      }
-#endif
     }
 #ifdef TF_TRACE
     if (tid == 0 && blockIdx.x < kTrCtas) {
@@ -1805,7 +1812,7 @@ static bool pdl_enabled() {
 template <int MODE, int VW, int IN, int OUT>
 static int launch(const CapParams& P, int grid, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(grid + 1);  // + the controller CTA (blockIdx 0)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
