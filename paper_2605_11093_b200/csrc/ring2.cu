@@ -1916,8 +1916,9 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
     waves = e ? std::max(1, atoi(e)) : 1;
   }
   const uint64_t chunk = uint64_t(chunk_kb) << 10;
+  // (- 1: the controller CTA the launch adds keeps the whole grid resident)
   int grid_bytes = int(std::min<uint64_t>((out_max + chunk - 1) / chunk,
-                                          uint64_t(g_sm_count) * kCtasPerSm * waves));
+                                          uint64_t(g_sm_count) * kCtasPerSm * waves - 1));
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
   int grid = std::max(1, std::max(grid_bytes, grid_table));
   if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));
