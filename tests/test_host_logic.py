@@ -298,3 +298,29 @@ def test_binary_prefix_search_equals_linear_scan():
                 linear = m
                 break
         assert len(plan.kept_ids) == linear
+
+
+def test_plan_entries_cache_follows_filter_and_tokens():
+    reg = install_hooks(ModelSpec(2, 16), [
+        HookSpec("resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+        HookSpec("logits", ("tokens", 8), DType.of("f32"))])
+    e = reg.plan_entries(3)
+    assert [(h, hk.name, sh) for h, hk, sh in e] == [
+        (i, reg.hook(i).name, reg.hook(i).resolve_shape(3, 16)) for i in reg.enabled_ids()]
+    assert reg.plan_entries(3) is e
+    reg.set_hook_filter(["logits"])
+    reg.commit_filter()
+    assert [hk.name for _, hk, _ in reg.plan_entries(3)] == ["logits"]
+    assert reg.plan_entries(5)[0][2] == (5, 8)
+
+
+def test_with_hook_equals_full_construction():
+    from paper_2605_11093_b200 import TensorMeta
+    base = TensorMeta("a[0]", 0, 7, (3, 1), ((0, 2), (5, 9)), (4, 16), DType.of("bf16"),
+                      (1, 0), row_counts=(2, 4))
+    m = base.with_hook("b[1]", 1, (4, 32), DType.of("f32"))
+    full = TensorMeta("b[1]", 1, 7, (3, 1), ((0, 2), (5, 9)), (4, 32), DType.of("f32"),
+                      (1, 0), row_counts=(2, 4))
+    assert m == full and m.expected_payload_len == full.expected_payload_len
+    with pytest.raises(ConfigError):
+        base.with_hook("c", 0, (0, 4), DType.of("u8"))
