@@ -330,9 +330,26 @@ class ExportPipeline:
         self.pageable_bytes_in_flight -= total
         return total
 
+    @staticmethod
+    def _wants_captures(sink) -> bool:
+        """Whole-batch fast path only when the sink's ``write_captures`` is
+        at least as specific as its ``write`` (a subclass that overrides
+        ``write`` alone, e.g. a collecting NullSink, keeps the records
+        path)."""
+        wc = getattr(sink, "write_captures", None)
+        if wc is None:
+            return False
+        mro = type(sink).__mro__
+        def owner(name):
+            return next((c for c in mro if name in c.__dict__), None)
+        w_owner, c_owner = owner("write"), owner("write_captures")
+        if c_owner is None:  # instance attribute
+            return True
+        return w_owner is None or issubclass(c_owner, w_owner)
+
     def sink_batch(self, batch: PageableBatch, sink, now: float = 0.0) -> None:
         total = 0
-        if getattr(sink, "write_captures", None) is not None:
+        if self._wants_captures(sink):
             total = self._sink_captures(batch, sink, now)
             self.batches_sunk += 1
             self.events.append(DrainEvent(now, "sunk", batch.reason,

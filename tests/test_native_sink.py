@@ -124,3 +124,25 @@ def test_length_mismatch_is_meta_mismatch(tmp_path):
     with NativeFileSink(tmp_path / "ds") as s:
         with pytest.raises(MetaMismatch):
             s.write_captures([(meta, b"x" * 7, None)])
+
+
+def test_exporter_uses_batch_path_only_for_sinks_that_define_it(tmp_path):
+    from paper_2605_11093_b200.exporter import ExportPipeline
+    from paper_2605_11093_b200.sinks import NullSink
+
+    class Collect(NullSink):          # overrides write only: records path
+        def write(self, recs):
+            pass
+
+    class Both(NullSink):
+        def write(self, recs):
+            pass
+
+        def write_captures(self, caps):
+            pass
+
+    want = ExportPipeline._wants_captures
+    assert want(NullSink()) and not want(Collect()) and want(Both())
+    assert not want(FileSink(tmp_path / "a"))
+    with NativeFileSink(tmp_path / "b") as s:
+        assert want(s)
