@@ -746,6 +746,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     snap_load(P, sr);
     step = P.step_ptr ? *P.step_ptr : P.step_imm;
   }
+  // The keep bytes of a small keep vector are loaded before the speculative
+  // segment: memory requests leave the SM roughly in issue order, and the
+  // plan (which waits on them) must not queue behind megabytes of reads.
+  const bool small = P.keep && U <= 32;
+  const uint32_t kbyte = (small && warp == 0 && lane < U) ? P.keep[lane] : 0u;
   // COPY: speculatively load this warp's first segment of the
   // grid-interleaved order assuming every unit is kept (identity row map),
   // so the source read overlaps the keep/snapshot round trip; used only if
@@ -782,10 +787,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   uint64_t K;
   // <= 32 keep units (request keep): one warp, one coalesced load, ranks by
   // ballot; the whole rank table is built here and indexed from rank 0
-  const bool small = P.keep && U <= 32;
   if (small) {
     if (warp == 0) {
-      const uint32_t k = lane < U ? P.keep[lane] : 0u;
+      const uint32_t k = kbyte;
       const uint32_t m = __ballot_sync(0xffffffffu, k != 0);
       if (k) sh.table[__popc(m & ((1u << lane) - 1u))] = (uint32_t)lane;
       if (lane == 0) sh.total = __popc(m);

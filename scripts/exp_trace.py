@@ -44,7 +44,7 @@ def trace(n):
         g = int(pub[slot, 1])
         if g == 0:
             continue
-        st = stamps[slot, :g].astype(np.int64)
+        st = stamps[slot, 1:g].astype(np.int64)  # CTA 0 is the controller (no copy stamps)
         e0 = st[:, 0].min()
         rows.append(((st[:, 0].max() - e0), (st[:, 1].max() - e0), (st[:, 2].max() - e0),
                      (int(pub[slot, 0]) - e0), (st[:, 3].max() - e0), (st[:, 4].max() - e0),
