@@ -25,5 +25,5 @@ def run(n):
 run(50)
 print("begin+end us/step:", round(run(500), 1))
 pr = cProfile.Profile(); pr.enable(); run(300); pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(22)
 obs.close()
