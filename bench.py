@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--staging", default="copy-engine",
                    choices=["copy-engine", "mapped"])
     p.add_argument("--legs", default="value,e2e,model,cpu")
-    p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--page-out", default="handoff",
                    choices=["copy", "handoff"],
                    help="exporter page-out for the e2e and model legs")
