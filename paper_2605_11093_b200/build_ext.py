@@ -68,6 +68,8 @@ def build(force: bool = False, verbose: bool = False,
                 defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")
             elif part.startswith("u"):
                 defines.append(f"-DTF_UNROLL={int(part[1:])}")
+            elif part == "nospec0":
+                defines.append("-DTF_SPEC_WARP0=0")
     for src in SOURCES:
         obj = LIB_DIR / (Path(src).stem + (f"_{variant}" if variant else "") + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", str(ROOT / "include"), "-c",

@@ -762,7 +762,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     if (!(TF_ABL & 256) && (!P.keep || U <= 32)) {
       const int64_t spr0 = (P.words_per_row + kSeg - 1) / kSeg;
       const int64_t s0 = int64_t(cb) * kWarps + warp;
-      if (cb >= 0 && s0 < U * P.rpu * spr0) {
+#ifndef TF_SPEC_WARP0
+#define TF_SPEC_WARP0 1
+#endif
+      // (TF_SPEC_WARP0=0: warp 0, which runs the plan, skips the speculative
+      // load so its memory queue stays empty; A/B builds)
+      if (cb >= 0 && (TF_SPEC_WARP0 || warp != 0) && s0 < U * P.rpu * spr0) {
         const int64_t j0 = qdiv(s0, spr0);
         const int64_t k0 = (s0 - j0 * spr0) * kSeg;
         const int64_t k1 = imin64(k0 + kSeg, P.words_per_row);
