@@ -47,15 +47,11 @@ from vllm.v1.worker.gpu_worker import Worker
 from .exporter import DrainConfig
 from .hookpoint import HookPoint, Observer
 from .hooks import DType, HookSpec, ModelSpec, install_hooks
-from .policy import BEST_EFFORT, COMPLETENESS, PolicyConfig, StepRequest
+from .policy import BEST_EFFORT, COMPLETENESS, DROP_RECENT, PolicyConfig, StepRequest
 from .rings import RingConfig
 from .sinks import NullSink
 
 ENV = "TF_VLLM_OBSERVER"
-
-
-def _first(x):
-    return x[0] if isinstance(x, (tuple, list)) else x
 
 
 def vllm_llama_specs(hf_config, sites, dtype: str = "bf16") -> list[HookSpec]:
@@ -187,8 +183,11 @@ class ObservedWorker(Worker):
         sched = self.vllm_config.scheduler_config
         max_tokens = int(sched.max_num_batched_tokens)
         max_seqs = int(sched.max_num_seqs)
-        policy = PolicyConfig(mode=BEST_EFFORT if cfg["policy"] == "best-effort"
-                              else COMPLETENESS)
+        if cfg["policy"] == "best-effort":  # drop-recent unless configured
+            policy = PolicyConfig(mode=BEST_EFFORT,
+                                  strategy=cfg.get("strategy", DROP_RECENT))
+        else:
+            policy = PolicyConfig(mode=COMPLETENESS)
         self._tf_sink = ListSink() if cfg.get("sink") == "list" else CountingSink()
         obs = Observer(
             reg, ring=RingConfig(int(cfg["ring_bytes"]), int(cfg["meta_slots"])),
@@ -203,7 +202,8 @@ class ObservedWorker(Worker):
         obs.start()
         self._tf_obs = obs
         self._tf_handles = attach_vllm_llama(model, obs, sites)
-        self._tf_req = {}        # vLLM request id -> (int id, arrival index)
+        self._tf_req = {}        # live vLLM request id -> int id (= arrival index)
+        self._tf_next_id = 0
         self._tf_step = 0
         self._tf_layouts = {}    # debug: step -> [(request id, rows)]
         self._tf_clones = []
@@ -238,6 +238,8 @@ class ObservedWorker(Worker):
         rows_total = (input_ids if input_ids is not None else positions).shape[0]
         batch = []
         if so is not None:
+            for rid in getattr(so, "finished_req_ids", ()):  # ids of finished requests
+                self._tf_req.pop(rid, None)
             ib = self.model_runner.input_batch
             sched = so.num_scheduled_tokens
             for rid in ib.req_ids:
@@ -245,11 +247,12 @@ class ObservedWorker(Worker):
                 if n <= 0:
                     continue
                 ent = self._tf_req.get(rid)
-                if ent is None:
-                    ent = (len(self._tf_req), len(self._tf_req))
+                if ent is None:  # first sight: next arrival index
+                    ent = self._tf_next_id
+                    self._tf_next_id += 1
                     self._tf_req[rid] = ent
                 start = int(ib.num_computed_tokens_cpu[ib.req_id_to_index[rid]])
-                batch.append(StepRequest(ent[0], ent[1], "", int(n), start))
+                batch.append(StepRequest(ent, ent, "", int(n), start))
         # dummy / warm-up forwards get an empty batch: every row dropped
         obs.begin_step(batch, self._tf_step, layout="flat", rows_total=rows_total)
         if self._tf_cfg.get("debug_clone") or self._tf_cfg.get("sink") == "list":
