@@ -39,7 +39,7 @@ from .errors import ConfigError, PolicyUnderestimate
 from .exporter import DrainConfig, ExportPipeline
 from .hooks import HookRegistry, RowSource, capture_args, launch_capture
 from .policy import COMPLETENESS, PolicyConfig, StepPlan, prepare_step
-from .records import TensorMeta, TensorMetaFIFO
+from .records import StepMetas, TensorMeta, TensorMetaFIFO
 from .rings import RingConfig, RingPair
 
 nn = torch().nn
@@ -186,14 +186,16 @@ class Observer:
                                 ragged=flat)
             if self.policy.mode == COMPLETENESS:
                 st, t0, since, big = self._sc
-                for m in plan.fifo_entries:
-                    n = m.expected_payload_len
+                fe = plan.fifo_entries
+                lens = fe.payload_lens() if isinstance(fe, StepMetas) else \
+                    [m.expected_payload_len for m in fe]
+                for n in lens:
                     since += n + 16
                     big = max(big, n)
                 self._sc = (st, t0, since, big)
         if plan.flush_before:
             self.flush()
-        metas = list(plan.fifo_entries)
+        metas = plan.fifo_entries
         sel = {}
         kept_set = set(plan.kept_ids)
         if self.sampler is not None and plan.kept_ids and self.sampled_hooks:

@@ -324,3 +324,24 @@ def test_with_hook_equals_full_construction():
     assert m == full and m.expected_payload_len == full.expected_payload_len
     with pytest.raises(ConfigError):
         base.with_hook("c", 0, (0, 4), DType.of("u8"))
+
+
+def test_step_metas_fifo_materialises_lazily_in_order():
+    from paper_2605_11093_b200 import TensorMeta, TensorMetaFIFO
+    from paper_2605_11093_b200.records import StepMetas
+    bf = DType.of("bf16")
+    base = TensorMeta("a[0]", 0, 3, (5, 2), ((0, 4), (1, 2)), (4, 8), bf, row_counts=(4, 1))
+    sm = StepMetas(base, [("a[0]", 0, (4, 8), bf), ("b[0]", 0, (4, 16), bf),
+                          ("c", None, (4, 2), DType.of("f32"))])
+    assert sm._cache[1] is None and len(sm) == 3
+    assert sm.payload_lens() == [m.expected_payload_len for m in sm]
+    fifo = TensorMetaFIFO()
+    fifo.push(TensorMeta("z", 0, 2, (9,), ((0, 1),), (1, 4), bf))
+    fifo.extend(sm)
+    assert len(fifo) == 4
+    d = lambda name, n: Descriptor(0, n, 0, 3 if name != "z" else 2)  # noqa: E731
+    assert fifo.match(d("z", 8), "z").hook_name == "z"
+    assert fifo.peek().hook_name == "a[0]"
+    for m in sm:
+        assert fifo.match(d(m.hook_name, m.expected_payload_len), m.hook_name) == m
+    assert len(fifo) == 0 and fifo.peek() is None
