@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+from collections import deque
 import time
 from dataclasses import dataclass, field
 
@@ -34,6 +35,9 @@ from .rings import Descriptor, RingPair
 STAGE_QUEUE_SLOTS = 16
 STAGING_MODES = {"copy-engine": N.TF_STAGE_COPY_ENGINE,
                  "mapped": N.TF_STAGE_MAPPED}
+
+
+EVENT_LOG_MAX = 1 << 16
 
 
 @dataclass(frozen=True)
@@ -188,7 +192,9 @@ class ExportPipeline:
         N.check(N.lib().tf_stager_create(ring.handle, C.byref(cfg), C.byref(st)))
         self._st = st
         self.pool = StagingPool(self)
-        self.events: list[DrainEvent] = []
+        # the event log (exporter.py:98-121) is bounded: a serving process
+        # sinks batches for hours
+        self.events: deque = deque(maxlen=EVENT_LOG_MAX)
         self.pageable_bytes_in_flight = 0
         self.max_transient_bytes = 0
         self.batches_drained = 0

@@ -191,7 +191,12 @@ class ObservedWorker(Worker):
         self._tf_sink = ListSink() if cfg.get("sink") == "list" else CountingSink()
         obs = Observer(
             reg, ring=RingConfig(int(cfg["ring_bytes"]), int(cfg["meta_slots"])),
-            drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1, max_wait=1e-4,
+            # reference-sized drain batches (exporter.py:35-51 defaults are
+            # 8 entries / 1 MiB / 2 ms): one sink-thread pass per many
+            # captures keeps the exporter's Python off the engine's GIL
+            drain=DrainConfig(min_ready_entries=int(cfg.get("drain_entries", 32)),
+                              min_ready_bytes=int(cfg.get("drain_bytes", 4 << 20)),
+                              max_wait=float(cfg.get("drain_wait", 2e-3)),
                               staging_buffer_size=int(cfg["staging_buffer_mib"]) << 20,
                               staging_buffer_count=int(cfg["staging_buffers"]),
                               page_out="handoff"),
