@@ -59,7 +59,7 @@ from .policy import (
     estimate_step_bytes,
     prepare_step,
 )
-from .records import CaptureRecord, TensorMeta, TensorMetaFIFO
+from .records import CaptureRecord, StepMetas, TensorMeta, TensorMetaFIFO
 from .rings import (
     COPY_UNIT,
     DESCRIPTOR_SIZE,
@@ -74,6 +74,8 @@ from .rings import (
 )
 from .sinks import (
     FileSink,
+    NativeFileSink,
+    NativeStreamSink,
     NullSink,
     StreamSink,
     read_dataset,
