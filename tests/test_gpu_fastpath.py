@@ -132,3 +132,25 @@ def test_tiny_meta_ring_forces_leader_path():
     got, want, state, counters, _ = _stream(5, 120, 1 << 20, 2, max_bytes=20_000)
     assert got == want
     assert state.occupancy == 0
+
+
+def test_huge_token_keep_uses_inline_publish_path():
+    """> 512 copy CTAs (a 1.2 M-row token keep needs ~590 rank-table slices):
+    the fast path falls back to the last-CTA publish; bytes must match the
+    reference gather and the ring must drain empty."""
+    torch.manual_seed(3)
+    rows, row = 1_200_000, 16
+    x = torch.randint(0, 256, (rows, row), dtype=torch.uint8, device="cuda")
+    keep = (torch.rand(rows, device="cuda") < 0.5).to(torch.uint8)
+    ring = RingPair(RingConfig(payload_capacity=64 << 20, meta_slots=16))
+    src = RowSource(x.data_ptr(), rows, 1, row, row, row, x)
+    launch_capture(ring, capture_args(src, hook_id=0, keep_ptr=keep.data_ptr(),
+                                      step_seq=5, full="raise"), torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    (d,) = ring.poll_ready(1)
+    want = x[keep.bool()].cpu().numpy().tobytes()
+    assert d.payload_len == len(want)
+    assert bytes(ring.payload_view(d.payload_offset, d.payload_len)) == want
+    assert (d.flags >> 16) == 0
+    ring.release_payload(d.payload_offset, round_up_to_copy_unit(d.payload_len))
+    ring.close()
