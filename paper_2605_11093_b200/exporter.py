@@ -444,6 +444,12 @@ class ExportPipeline:
         n = pb.n_entries
         raw = (C.c_char * max(1, pb.bytes_total)).from_address(pb.payload)
         view = memoryview(raw).cast("B")
+        if n and self._wants_captures(self._sink):
+            # a raise (MetaMismatch) leaves the batch to _sink_loop to free
+            self._sink_paged_captures(pb, n, view)
+            del view
+            lib.tf_stager_free_paged(self._st, C.byref(pb))
+            return
         batch = PageableBatch(reason=N.REASONS.get(pb.reason, "none"))
         for i in range(n):
             d = Descriptor.from_c(pb.descs[i])
@@ -455,6 +461,45 @@ class ExportPipeline:
             self._sunk_batches_bg += 1
         del batch, view
         lib.tf_stager_free_paged(self._st, C.byref(pb))
+
+    def _sink_paged_captures(self, pb, n: int, view) -> None:
+        """Background fast path for batch sinks: the batch's descriptors are
+        read as columns in one step and matched against the metadata FIFO
+        without per-descriptor Python objects (the sink thread shares the
+        GIL with the inference engine)."""
+        import numpy as np
+        cols = np.ctypeslib.as_array(pb.descs, shape=(n,))
+        hooks = cols["hook_id"].tolist()
+        steps = cols["step_seq"].tolist()
+        lens = cols["payload_len"].tolist()
+        starts = np.ctypeslib.as_array(pb.starts, shape=(n,)).tolist()
+        base = pb.payload
+        name_of = self._hook_name_of
+        match = self.fifo.match_raw
+        caps = []
+        total = recs = 0
+        for i in range(n):
+            ln = lens[i]
+            meta = match(steps[i], name_of(hooks[i]), ln)
+            st = starts[i]
+            caps.append((meta, view[st:st + ln], base + st))
+            total += ln
+            recs += len(meta.request_ids)
+        now = time.monotonic()
+        with self._lock:
+            try:
+                self._sink.write_captures(caps)
+            except Exception as exc:  # sink faults are isolated (exporter.py:266-271)
+                self.sink_failures += 1
+                self.events.append(DrainEvent(now, "sink-error", str(exc), recs, total))
+            else:
+                self.records_out += recs
+                self.bytes_out += total
+            self.batches_sunk += 1
+            self.events.append(DrainEvent(now, "sunk", N.REASONS.get(pb.reason, "none"),
+                                          n, total))
+            self._sunk_batches_bg += 1
+        del caps
 
     def stream_handle(self) -> int:
         """cudaStream_t of the staging D2H work (for cross-stream events)."""
