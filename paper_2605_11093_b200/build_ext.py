@@ -70,6 +70,8 @@ def build(force: bool = False, verbose: bool = False,
                 defines.append(f"-DTF_UNROLL={int(part[1:])}")
             elif part == "nospec0":
                 defines.append("-DTF_SPEC_WARP0=0")
+            elif part.startswith("smem"):  # trace_smemN: N shared-memory spec segments
+                defines.append(f"-DTF_SMEM_SPEC={int(part[4:])}")
     for src in SOURCES:
         obj = LIB_DIR / (Path(src).stem + (f"_{variant}" if variant else "") + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", str(ROOT / "include"), "-c",

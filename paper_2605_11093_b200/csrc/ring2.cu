@@ -171,6 +171,13 @@ constexpr int kTableMax = 2048;
 #endif
 constexpr int kUnroll = TF_UNROLL;
 constexpr int kSeg = 32 * kUnroll;  // vector words per warp segment
+#ifndef TF_SMEM_SPEC
+#define TF_SMEM_SPEC 2
+#endif
+// COPY with 16-B words: segments 2..(1+kSmemSpec) of each warp are also
+// fetched before the plan, into shared memory with cp.async
+constexpr int kSmemSpec = TF_SMEM_SPEC;
+constexpr int kSpecSmemBytes = kSmemSpec * 8 /*warps*/ * kSeg * 16;
 #ifndef TF_CTAS_PER_SM
 #define TF_CTAS_PER_SM 2
 #endif
@@ -540,6 +547,12 @@ __device__ __forceinline__ bool fast_plan(const CapParams& P, const SnapRegs& r,
   return true;
 }
 
+__device__ __forceinline__ void cpa16(uint32_t smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Fast path, thread 0 of the publishing CTA: the 64-B descriptor of this
 // capture. With completion flags (n_ctas > 0) it is posted as soon as the
 // plan is known; the host takes the slot only when all n_ctas CTAs have set
@@ -716,6 +729,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // CTA 0 is the controller: it posts the descriptor and commits the
   // producer state while the others copy; copy CTA cb of cg owns the work.
   const int cb = int(blockIdx.x) - 1, cg = int(gridDim.x) - 1;
+  extern __shared__ __align__(16) uint4 spec_smem[];  // COPY/16: kSpecSmemBytes
   const int64_t U = P.units;
   const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
 #ifdef TF_TRACE
@@ -778,6 +792,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
         }
         spec_s = s0;
+        if constexpr (VW == 16 && kSmemSpec > 0) {
+          // the warp's next segments of the grid-interleaved order, into its
+          // shared-memory slots (each lane later reads back its own words)
+          const int64_t sstep = int64_t(cg) * kWarps;
+          const int64_t all = U * P.rpu * spr0;
+#pragma unroll
+          for (int t = 0; t < kSmemSpec; ++t) {
+            const int64_t sn = s0 + (t + 1) * sstep;
+            if (sn < all) {
+              const int64_t jn = qdiv(sn, spr0);
+              const int64_t kn0 = (sn - jn * spr0) * kSeg;
+              const int64_t kn1 = imin64(kn0 + kSeg, P.words_per_row);
+              const uint8_t* srcn = row_src(P, jn);
+              uint4* slot = spec_smem + (size_t(t) * kWarps + warp) * kSeg;
+#pragma unroll
+              for (int i = 0; i < kUnroll; ++i) {
+                int64_t k = kn0 + lane + i * 32;
+                if (k < kn1)
+                  cpa16(static_cast<uint32_t>(__cvta_generic_to_shared(slot + lane + i * 32)),
+                        srcn + k * 16);
+              }
+            }
+          }
+          cpa_commit();
+        }
       }
     }
   }
@@ -980,8 +1019,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #ifdef TF_TRACE
     if (tid == 0) t_plan = globaltimer();
 #endif
+    // the shared-memory speculation holds iff the register one does (same
+    // identity map, same interleaved order)
+    const bool smem_ok = VW == 16 && kSmemSpec > 0 && spec_s == s && K == (uint64_t)U;
     if (sh.status == TF_OK && s < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
+      int it = 0;
       for (;;) {
         uint8_t* dst = dst_base + j * P.out_row_bytes;
 #pragma unroll
@@ -990,18 +1033,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
         }
         s += s_step;
+        ++it;
         if (s >= s_end) break;
         j = qdiv(s, spr);
         k0 = (s - j * spr) * kSeg;
         k1 = imin64(k0 + kSeg, wpr);
-        const uint8_t* src = row_src(P, row_of(j));
+        if (smem_ok && it <= kSmemSpec) {
+          if constexpr (VW == 16 && kSmemSpec > 0) {
+            cpa_wait_all();
+            const uint4* slot = spec_smem + (size_t(it - 1) * kWarps + warp) * kSeg;
 #pragma unroll
-        for (int i = 0; i < kUnroll; ++i) {
-          int64_t k = k0 + lane + i * 32;
-          if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+            for (int i = 0; i < kUnroll; ++i) {
+              int64_t k = k0 + lane + i * 32;
+              if (k < k1) v[i] = slot[lane + i * 32];
+            }
+          }
+        } else {
+          const uint8_t* src = row_src(P, row_of(j));
+#pragma unroll
+          for (int i = 0; i < kUnroll; ++i) {
+            int64_t k = k0 + lane + i * 32;
+            if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
+          }
         }
       }
     }
+    if constexpr (VW == 16 && kSmemSpec > 0) cpa_wait_all();  // no copy left in flight
   } else {
     if (tid == 0 && !fast) {
       if (!leader)
@@ -1739,6 +1796,13 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     return fail(TF_ERR_CUDA);
   }
   r->snap_stream = s;
+  if (kSmemSpec > 0 && kSpecSmemBytes > 48 * 1024 &&
+      cudaFuncSetAttribute(capture_kernel<MODE_COPY, 16, 0, 0>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSpecSmemBytes) != cudaSuccess) {
+    tf_set_error("shared-memory opt-in failed");
+    return fail(TF_ERR_CUDA);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TF_ERR_CUDA);
   *out = r;
   return TF_OK;
@@ -1820,10 +1884,13 @@ static bool pdl_enabled() {
 
 template <int MODE, int VW, int IN, int OUT>
 static int launch(const CapParams& P, int grid, cudaStream_t s) {
+  // (the >48 KiB opt-in is set once per device in tf_ring_create, outside
+  // any stream capture)
+  constexpr int smem = (MODE == MODE_COPY && VW == 16 && kSmemSpec > 0) ? kSpecSmemBytes : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid + 1);  // + the controller CTA (blockIdx 0)
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
