@@ -763,8 +763,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // The keep bytes of a small keep vector are loaded before the speculative
   // segment: memory requests leave the SM roughly in issue order, and the
   // plan (which waits on them) must not queue behind megabytes of reads.
-  const bool small = P.keep && U <= 32;
-  const uint32_t kbyte = (small && warp == 0 && lane < U) ? P.keep[lane] : 0u;
+  // <= 256 keep units (request keep, or the token rows of a decode step):
+  // one byte per thread, ranks by warp ballots, the whole rank table in
+  // shared memory
+  const bool small = P.keep && U <= kThreads;
+  const uint32_t kbyte = (small && tid < U) ? P.keep[tid] : 0u;
   // COPY: speculatively load this warp's first segment of the
   // grid-interleaved order assuming every unit is kept (identity row map),
   // so the source read overlaps the keep/snapshot round trip; used only if
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   CV v[kUnroll];
   int64_t spec_s = -1;
   if constexpr (MODE == MODE_COPY) {
-    if (!(TF_ABL & 256) && (!P.keep || U <= 32)) {
+    if (!(TF_ABL & 256) && (!P.keep || U <= kThreads)) {
       const int64_t spr0 = (P.words_per_row + kSeg - 1) / kSeg;
       const int64_t s0 = int64_t(cb) * kWarps + warp;
 #ifndef TF_SPEC_WARP0
@@ -831,15 +834,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   uint64_t K;
   // <= 32 keep units (request keep): one warp, one coalesced load, ranks by
   // ballot; the whole rank table is built here and indexed from rank 0
+  bool prefix = !P.keep;  // kept units are exactly units [0, K): identity map
   if (small) {
-    if (warp == 0) {
-      const uint32_t k = kbyte;
-      const uint32_t m = __ballot_sync(0xffffffffu, k != 0);
-      if (k) sh.table[__popc(m & ((1u << lane) - 1u))] = (uint32_t)lane;
-      if (lane == 0) sh.total = __popc(m);
-    }
+    const uint32_t m = __ballot_sync(0xffffffffu, kbyte != 0);
+    if (lane == 0) sh.warp_sums[warp] = __popc(m);
     __syncthreads();
-    K = sh.total;
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = sh.warp_sums[w];
+      base += w < warp ? c : 0u;
+      tot += c;
+    }
+    if (kbyte) sh.table[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)tid;
+    K = tot;
+    // a prefix of ones (e.g. a graph-padded token layout) keeps the identity
+    // row map, so the speculative segments stay valid
+    prefix = __syncthreads_and(tid >= U || ((kbyte != 0) == (uint32_t(tid) < tot))) != 0;
     TSTAMP(t_scan);
   } else if (P.keep) {
     int64_t per = (U + kThreads - 1) / kThreads;
@@ -998,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       j = qdiv(s, spr);
       k0 = (s - j * spr) * kSeg;
       k1 = imin64(k0 + kSeg, wpr);
-      if (!(spec_s == s && K == (uint64_t)U)) {
+      if (!(spec_s == s && prefix)) {
         const uint8_t* src = row_src(P, row_of(j));
 #pragma unroll
         for (int i = 0; i < kUnroll; ++i) {
@@ -1021,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #endif
     // the shared-memory speculation holds iff the register one does (same
     // identity map, same interleaved order)
-    const bool smem_ok = VW == 16 && kSmemSpec > 0 && spec_s == s && K == (uint64_t)U;
+    const bool smem_ok = VW == 16 && kSmemSpec > 0 && spec_s == s && prefix;
     if (sh.status == TF_OK && s < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
       int it = 0;

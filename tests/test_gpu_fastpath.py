@@ -154,3 +154,35 @@ def test_huge_token_keep_uses_inline_publish_path():
     assert (d.flags >> 16) == 0
     ring.release_payload(d.payload_offset, round_up_to_copy_unit(d.payload_len))
     ring.close()
+
+
+@pytest.mark.parametrize("pattern", ["prefix", "all", "none_kept_tail", "holes"])
+def test_token_row_keep_up_to_256_rows(pattern):
+    """<= 256 keep units take the ballot path with speculative loads; a keep
+    vector that is a prefix of ones (CUDA-graph padding rows at the end)
+    keeps the speculation valid, any other pattern must fall back."""
+    torch.manual_seed(17)
+    rng = random.Random(17)
+    for rows, row in ((256, 8192), (200, 28672), (40, 4096), (256, 48), (97, 4000)):
+        x = torch.randint(0, 256, (rows, row), dtype=torch.uint8, device="cuda")
+        if pattern == "prefix":
+            n = rng.randint(1, rows)
+            keep = [1] * n + [0] * (rows - n)
+        elif pattern == "all":
+            keep = [1] * rows
+        elif pattern == "none_kept_tail":
+            keep = [0] * (rows // 2) + [1] * (rows - rows // 2)
+        else:
+            keep = [int(rng.random() < 0.6) for _ in range(rows)]
+            keep[0] = 1
+        kt = torch.tensor(keep, dtype=torch.uint8, device="cuda")
+        ring = RingPair(RingConfig(payload_capacity=64 << 20, meta_slots=16))
+        src = RowSource(x.data_ptr(), rows, 1, row, row, row, x)
+        launch_capture(ring, capture_args(src, hook_id=1, keep_ptr=kt.data_ptr(), step_seq=2,
+                                          full="raise"), torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        (d,) = ring.poll_ready(1)
+        want = x[kt.bool()].cpu().numpy().tobytes()
+        assert d.payload_len == len(want)
+        assert bytes(ring.payload_view(d.payload_offset, d.payload_len)) == want, (rows, row)
+        ring.close()
