@@ -258,9 +258,12 @@ class RingPair:
             pass
 
     def note_launch(self, stream=None) -> None:
-        """Remember the producer stream position for snapshot fencing."""
+        """Remember the producer stream position for snapshot fencing (one
+        event, re-recorded: a serving engine notes every step)."""
         t = torch()
-        ev = t.cuda.Event()
+        ev = getattr(self, "_note_ev", None)
+        if ev is None:
+            ev = self._note_ev = t.cuda.Event()
         ev.record(stream if stream is not None
                   else t.cuda.current_stream(self.device))
         self._pending = ev
