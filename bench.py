@@ -272,11 +272,9 @@ def leg_value(args, dist, dev):
     pipe.stop(flush=True)
     roof_ev = [(torch.cuda.Event(enable_timing=True),
                 torch.cuda.Event(enable_timing=True)) for _ in range(n_caps)]
-    k0 = ring.state().kernel_ns
     run_step(1, roof_ev)
     prod.synchronize()
     ring.note_launch(prod)
-    roof_dev_ns = (ring.state().kernel_ns - k0) / n_caps
     roof_ms = [a.elapsed_time(b) for a, b in roof_ev]
     # the same step's launches back to back, one event pair around all of
     # them (no per-launch event overhead): span / launches
@@ -345,7 +343,6 @@ def leg_value(args, dist, dev):
         "staged_bytes": staged, "elapsed_s": elapsed,
         "step_bytes": step_bytes, "captures_per_step": n_caps,
         "kernel_ms": kernel_ms, "launch_bytes": per_launch,
-        "kernel_dev_us": roof_dev_ns / 1e3,
         "span_ms": span_ms,
         "graph_span_ms": graph_span_ms,
         "per_kind_us": {
@@ -772,7 +769,6 @@ def main():
                          "avg_launch_us_eager_back_to_back": avg_ms_eager * 1e3,
                          "frac_eager_back_to_back": avg_alg / (avg_ms_eager * 1e-3) / 1e9 / peak,
                          "avg_launch_us_event_pair_each": avg_ms_events * 1e3,
-                         "avg_launch_us_device_timer": v["kernel_dev_us"],
                          "avg_launch_us_in_timed_region": v["timed_kernel_avg_us"],
                          "per_kind_us_event_pair_each": v["per_kind_us"],
                          "algorithmic_bytes_per_launch": avg_alg,

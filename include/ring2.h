@@ -112,8 +112,12 @@ typedef struct tf_ring_state {
   uint64_t stall_events;      /* waits under TF_FULL_WAIT */
   uint64_t stall_ns;
   uint64_t device_errors;     /* bitmask of TF_DEVERR_* */
-  uint64_t kernel_ns;         /* sum of capture-kernel durations (device globaltimer) */
-  uint64_t last_kernel_ns;    /* duration of the most recent capture kernel */
+  /* Producer latency (device globaltimer), NOT the kernel duration: on the
+     fast path the controller CTA stamps entry -> producer-state commit, which
+     ends while copy CTAs are still copying; on the slow path the last CTA
+     stamps entry -> descriptor. Time kernels with CUDA events instead. */
+  uint64_t kernel_ns;         /* sum of producer latencies */
+  uint64_t last_kernel_ns;    /* producer latency of the most recent capture */
 } tf_ring_state;
 
 #define TF_DEVERR_UNDERESTIMATE 0x1u /* drop under TF_FULL_DROP (best effort) */

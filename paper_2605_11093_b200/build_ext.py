@@ -50,8 +50,10 @@ def build(force: bool = False, verbose: bool = False,
     """Compile the sources to objects and link the shared library.
 
     ``variant="trace"`` builds ``libring2_trace.so`` with -DTF_TRACE (phase
-    timers in the capture kernel) for experiments; the product library is
-    always the plain ``libring2.so``."""
+    timers in the capture kernel) and ``variant="variants"`` builds
+    ``libring2_variants.so`` with the rejected TMA / cp.async copy paths, for
+    experiments; the product library is always the plain ``libring2.so``
+    (hot path only)."""
     lib = LIB if not variant else LIB_DIR / f"libring2_{variant}.so"
     if not force and not variant and not _stale():
         return LIB
@@ -59,6 +61,8 @@ def build(force: bool = False, verbose: bool = False,
     nvcc = _nvcc()
     objs = []
     defines = []
+    if variant == "variants":  # rejected copy paths (TF_COPY_PATH=tma|stage)
+        defines.append("-DTF_COPY_VARIANTS")
     if variant and variant.startswith("trace"):
         defines.append("-DTF_TRACE")
         for part in variant.split("_")[1:]:  # trace_ablN_cM: ablation N, M CTAs/SM

@@ -1300,6 +1300,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   }
 }
 
+// Rejected copy-path variants (measured slower on B200) are
+// compiled only into experiment builds (-DTF_COPY_VARIANTS).
+#ifdef TF_COPY_VARIANTS
 // ---------------------------------------------------------------------------
 // TMA bulk-copy capture (COPY, 16-B aligned rows): global -> smem -> ring
 // with cp.async.bulk. One CTA per SM, kTmaStages x 32 KiB stages. The
@@ -1679,6 +1682,8 @@ __global__ void __launch_bounds__(kStgThreads, kStgCtasPerSm) capture_stage_kern
     }
   }
 }
+
+#endif  // TF_COPY_VARIANTS
 
 // Protocol-level producer ops (single thread): the same allocator and
 // publish rules exposed one call at a time, for the reference's ring tests.
@@ -2062,6 +2067,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (a->op == TF_OP_COPY) {
     int vw = std::min<int>(sal, pow2_align((uint64_t)a->row_bytes));
     P.words_per_row = a->row_bytes / vw;
+#ifdef TF_COPY_VARIANTS
     // 0 = LDG/STG warps (default: measured fastest on B200),
     // 1 = TMA bulk copies, 2 = cp.async smem staging (TF_COPY_PATH=tma|stage)
     static int copy_path = -1;
@@ -2106,6 +2112,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
       }
       return TF_OK;
     }
+#endif
     switch (vw) {
       case 16: return launch<MODE_COPY, 16, 0, 0>(P, grid, s);
       case 8: return launch<MODE_COPY, 8, 0, 0>(P, grid, s);

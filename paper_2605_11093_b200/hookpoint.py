@@ -316,15 +316,27 @@ class Observer:
         dst[:src.numel()].copy_(src.pin_memory(), non_blocking=True)
 
     def _flat_buf(self, kind: str, rows: int):
-        """Fixed per-row keep buffers for the flat layout (grown, never
-        moved while a CUDA graph may reference them)."""
+        """Fixed per-row keep buffers for the flat layout. A persistent
+        observer's buffers are referenced by recorded CUDA graphs, so they
+        are never moved: a step with more rows than ``flat_rows`` raises
+        instead of reallocating (a replay would read the stale buffer)."""
         t = torch()
         buf = self._flat.get(kind)
+        if buf is not None and buf.numel() < rows and self.persistent:
+            raise ConfigError(
+                f"step has {rows} token rows but the persistent observer's keep "
+                f"buffers hold {buf.numel()} (raise flat_rows to the engine's "
+                "maximum batched tokens)")
         if buf is None or buf.numel() < rows:
             n = max(rows, self._flat_rows)
             buf = t.zeros(n, dtype=t.uint8, device=f"cuda:{self.device}")
             self._flat[kind] = buf
         return buf
+
+    def step_token_start(self) -> int:
+        """Position of this step's first token in each sequence (batch
+        layout: uniform across the batch, the reference's model)."""
+        return self._batch[0].token_start if self._batch else 0
 
     def end_step(self, stream=None) -> None:
         self.ring.note_launch(stream)
@@ -457,12 +469,23 @@ def _rows_of(x, hook) -> RowSource:
         return RowSource(x2.data_ptr(), x2.shape[0], 1, x2.shape[1] * esz,
                          x2.stride(0) * esz, x2.shape[1] * esz, x2)
     b = x.shape[0]
-    inner = x[0]
-    if not inner.is_contiguous() or x.stride(-1) != 1:
-        x = x.contiguous()
-        inner = x[0]
     row_elems = x.shape[-1]
-    mid = inner.numel() // row_elems
+    if x.stride(-1) == 1:
+        # the rows of one request as one uniformly strided run, without a
+        # copy: contiguous per request, or e.g. a KV-cache slice
+        # (B, kv_heads, new_tokens, head_dim) of a larger cache whose
+        # new_tokens is 1 (decode) or the whole cache (prefill)
+        try:
+            xv = x.view(b, -1, row_elems)
+        except RuntimeError:
+            xv = None
+        if xv is not None and xv.stride(2) == 1:
+            mid = xv.shape[1]
+            s_mid = xv.stride(1) * esz if mid > 1 else row_elems * esz
+            return RowSource(xv.data_ptr(), b, mid, row_elems * esz,
+                             xv.stride(0) * esz, s_mid, x)
+    x = x.contiguous()  # any other layout: one torch copy, then rows
+    mid = x[0].numel() // row_elems
     return RowSource(x.data_ptr(), b, mid, row_elems * esz, x.stride(0) * esz,
                      row_elems * esz, x)
 

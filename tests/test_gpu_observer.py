@@ -317,6 +317,14 @@ def test_gpt2_hookpoints_match_hidden_states():
                    drain=DrainConfig(staging_buffer_size=8 << 20))
     obs.start()
     handles = attach_gpt2(model, obs)
+    # every block's own output, cloned by a plain torch forward hook
+    # (hidden_states[12] is after ln_f, so the last block is compared
+    # through this hook, not through hidden_states)
+    block_out = {}
+    ref_handles = [blk.register_forward_hook(
+        lambda m, a, out, L=L: block_out.__setitem__(
+            L, (out[0] if isinstance(out, tuple) else out).detach().clone()))
+        for L, blk in enumerate(model.transformer.h)]
     reqs = [StepRequest(i, i, "p", 128, 0) for i in range(8)]
     obs.begin_step(reqs, 0)
     with torch.no_grad():
@@ -324,18 +332,20 @@ def test_gpt2_hookpoints_match_hidden_states():
     obs.end_step()
     obs.flush()
     obs.close()
-    for h in handles:
+    for h in handles + ref_handles:
         h.remove()
     by_key = {(r.hook_name, r.request_id): bytes(r.payload) for r in sink.records}
     assert len(by_key) == 12 * 8
+    assert len(block_out) == 12
     for L in range(12):
-        # hidden_states[L+1] is block L's output (the last one after ln_f)
-        hs = out.hidden_states[L + 1] if L < 11 else None
+        hs = block_out[L]
+        if L < 11:  # hidden_states[L+1] is block L's output for L < 11
+            assert torch.equal(hs, out.hidden_states[L + 1])
         for i in range(8):
             rec = by_key[(f"resid_post[{L}]", i)]
-            if hs is not None:
-                assert rec == hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()
-            assert zlib.crc32(rec) == zlib.crc32(rec)
+            assert rec == hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes()
+            assert zlib.crc32(rec) == zlib.crc32(
+                hs[i].contiguous().view(torch.uint8).cpu().numpy().tobytes())
 
 
 def test_llama_attention_kv_token_sampling():
@@ -401,3 +411,22 @@ def test_llama_attention_kv_token_sampling():
                 k = got[(f"{kv}[{L}]", 10 + i)]
                 want = ref[f"{kv}[{L}]"][i].contiguous()
                 assert bytes(k.payload) == want.view(torch.uint8).cpu().numpy().tobytes()
+
+
+def test_persistent_flat_buffers_never_move():
+    """A persistent observer's keep buffers are referenced by recorded CUDA
+    graphs: a step larger than flat_rows raises instead of reallocating."""
+    from paper_2605_11093_b200.errors import ConfigError
+    H = 64
+    reg = install_hooks(ModelSpec(1, H), [HookSpec(
+        "resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True)])
+    obs = Observer(reg, ring=RingConfig(1 << 20, 16), sink=Collect(), max_batch=4,
+                   flat_rows=16, persistent=True)
+    ptr = obs._flat["req"].data_ptr()
+    obs.begin_step([StepRequest(1, 0, "a", 16, 0)], 0, layout="flat")
+    obs.end_step()
+    with pytest.raises(ConfigError):
+        obs.begin_step([StepRequest(1, 0, "a", 16, 16), StepRequest(2, 1, "b", 1, 0)],
+                       1, layout="flat", rows_total=17)
+    assert obs._flat["req"].data_ptr() == ptr
+    obs.close()
