@@ -52,13 +52,18 @@ def parse():
     p.add_argument("--seq", type=int, default=512)
     p.add_argument("--staging", default="copy-engine",
                    choices=["copy-engine", "mapped"])
-    p.add_argument("--legs", default="value,e2e,model,cpu")
+    p.add_argument("--legs", default="value,e2e,model,c2,cpu")
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--page-out", default="handoff",
                    choices=["copy", "handoff"],
                    help="exporter page-out for the e2e and model legs")
     p.add_argument("--pinned-buffers", type=int, default=12,
                    help="pinned staging buffers of 128 MiB")
+    p.add_argument("--c2-batch", type=int, default=64)
+    p.add_argument("--c2-prefill", type=int, default=512)
+    p.add_argument("--c2-decode", type=int, default=128)
+    p.add_argument("--model-ring-mib", type=int, default=2048,
+                   help="payload ring of the model (overhead) leg")
     p.add_argument("--profile", action="store_true",
                    help="value leg only, short; for ncu launch lists")
     return p.parse_args()
@@ -306,6 +311,29 @@ def leg_value(args, dist, dev):
     ring.note_launch(prod)
     graph_span_ms = g0.elapsed_time(g1)
     del graph
+    # per kind: a graph of the step's 32 resid_post (32 MiB) launches, and
+    # one of its 32 mlp_act (112 MiB) launches, each replayed into an empty
+    # ring: the resid config's own roofline
+    kind_us = {}
+    for kind, label in ((0, "resid_post"), (1, "mlp_act")):
+        pipe.start(sink=None)
+        pipe.flush(120)
+        pipe.stop(flush=True)
+        gk = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(prod):
+            with torch.cuda.graph(gk, stream=prod):
+                for a, _ in cap_args[kind::2]:
+                    launch_capture(ring, a, prod)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(prod)
+        with torch.cuda.stream(prod):
+            gk.replay()
+        k1.record(prod)
+        prod.synchronize()
+        ring.note_launch(prod)
+        kind_us[label] = {"avg_launch_us": k0.elapsed_time(k1) * 1e3 / len(cap_args[kind::2]),
+                          "bytes_per_launch": cap_args[kind][1]}
+        del gk
     pipe.start(sink=None)
     for w in range(args.warmup):
         run_step(2 + w)
@@ -345,6 +373,7 @@ def leg_value(args, dist, dev):
         "kernel_ms": kernel_ms, "launch_bytes": per_launch,
         "span_ms": span_ms,
         "graph_span_ms": graph_span_ms,
+        "graph_kind_us": kind_us,
         "per_kind_us": {
             "resid_post_32MiB": 1e3 * sum(roof_ms[0::2]) / max(1, len(roof_ms[0::2])),
             "mlp_act_112MiB": 1e3 * sum(roof_ms[1::2]) / max(1, len(roof_ms[1::2]))},
@@ -436,7 +465,15 @@ def leg_e2e(args, dist, dev):
 # ---------------------------------------------------------------------------
 # leg: model inference overhead
 # ---------------------------------------------------------------------------
-def leg_model(args, dist, dev):
+def build_model(dev):
+    import torch
+
+    from paper_2605_11093_b200.integrations import llama3_8b_config, random_llama
+    with torch.cuda.device(dev):
+        return random_llama(llama3_8b_config(), device=str(dev))
+
+
+def leg_model(args, dist, dev, model):
     import torch
 
     from paper_2605_11093_b200 import (BEST_EFFORT, DROP_RECENT, DrainConfig,
@@ -448,8 +485,6 @@ def leg_model(args, dist, dev):
                                                     llama_registry, random_llama)
     B, T = args.batch, args.seq
     cfg = llama3_8b_config()
-    with torch.cuda.device(dev):
-        model = random_llama(cfg, device=str(dev))
     g = torch.Generator(device=dev).manual_seed(7)
     ids = torch.randint(0, cfg.vocab_size, (B, T), device=dev, generator=g)
     stream = torch.cuda.current_stream(dev)
@@ -479,12 +514,14 @@ def leg_model(args, dist, dev):
                 model.model(input_ids=ids, use_cache=False)
         return graph
 
-    def run(n, step_fn, obs=None, base=0):
+    def run(n, step_fn, obs=None, base=0, halves=False):
         """n back-to-back steps (the host plans step k+1 while the device
-        runs step k); device time over the whole region per step."""
+        runs step k); device time over the whole region per step, and
+        (halves=True) also over the second half only: once the ring has
+        filled, that is the steady-state step time."""
         torch.cuda.synchronize(dev)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        ev[0].record(stream)
         for s in range(n):
             if obs is not None:
                 plan = obs.begin_step(batch, base + s)
@@ -493,9 +530,13 @@ def leg_model(args, dist, dev):
             step_fn()
             if obs is not None:
                 obs.end_step(stream)
-        b.record(stream)
-        b.synchronize()
-        return a.elapsed_time(b) / n
+            ev[s + 1].record(stream)
+        ev[n].synchronize()
+        whole = ev[0].elapsed_time(ev[n]) / n
+        if not halves:
+            return whole
+        h = n // 2
+        return whole, ev[h].elapsed_time(ev[n]) / (n - h)
 
     tally = {"kept": 0, "dropped": 0}
 
@@ -507,8 +548,8 @@ def leg_model(args, dist, dev):
         g0 = make_graph() if mode == "graph" else None
         step0 = g0.replay if g0 is not None else fwd
         run(2, step0)
-        base = run(n, step0)
-        res = {"no_capture_ms": base}
+        base, base_half = run(n, step0, halves=True)
+        res = {"no_capture_ms": base, "no_capture_ms_second_half": base_half}
         cases = [("resid", ("resid_post",), PolicyConfig()),
                  ("resid_mlp", ("mlp_act", "resid_post"), PolicyConfig())]
         if mode == "graph":  # overload regime under the best-effort policy
@@ -518,7 +559,11 @@ def leg_model(args, dist, dev):
             reg = llama_registry(cfg, sites)
             step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
             sink = NullSink()
-            obs = Observer(reg, ring=RingConfig(min(24 * GiB, 4 * step_bytes), 1024),
+            # the paper's 2 GB ring: it holds at most ~2
+            # steps of backlog, so a 20-step run reaches the steady state
+            # (PCIe-bound when a step's bytes exceed the link's share)
+            ring_bytes = args.model_ring_mib << 20
+            obs = Observer(reg, ring=RingConfig(ring_bytes, 1024),
                            drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
                                              max_wait=1e-4,
                                              staging_buffer_size=128 << 20,
@@ -540,7 +585,8 @@ def leg_model(args, dist, dev):
             run(max(1, args.warmup - 1), step1, obs, 100)
             obs.flush(300)
             tally["kept"] = tally["dropped"] = 0
-            t = run(n, step1, obs, 1000)   # run time stops at inference end
+            # run time stops at inference end (simulator.py:16-20, 449)
+            t, t_half = run(n, step1, obs, 1000, halves=True)
             t_tail = time.perf_counter()
             obs.flush(600)                 # export tail, reported apart
             t_tail = time.perf_counter() - t_tail
@@ -551,6 +597,11 @@ def leg_model(args, dist, dev):
             del g1
             res[label] = {
                 "capture_ms": t, "overhead_pct": (t - base) / base * 100.0,
+                "capture_ms_second_half": t_half,
+                "overhead_pct_steady": (t_half - base_half) / base_half * 100.0,
+                "overhead_pct_incl_export_tail":
+                    (t + t_tail * 1e3 / n - base) / base * 100.0,
+                "ring_bytes": ring_bytes, "steps": n,
                 "step_bytes": step_bytes, "policy": policy.mode,
                 "stall_events": st.stall_events,
                 "dropped_request_steps": tally["dropped"],
@@ -559,9 +610,101 @@ def leg_model(args, dist, dev):
                 "records": sink.records_written}
         del g0
         results[mode] = res
-    del model
     torch.cuda.empty_cache()
     return results
+
+
+# ---------------------------------------------------------------------------
+# leg: SURVEY C2 offline batch -- 64 x 512 prefill, then 128 decode steps
+# ---------------------------------------------------------------------------
+def leg_c2(args, dist, dev, model):
+    """64 prompts x 512 tokens of prefill (one mlp_act
+    capture is 896 MiB: staged in 128 MiB chunks, split_oversize), then
+    ``--c2-decode`` decode steps of 64 tokens (the fixed-cost regime: 64
+    captures of 512 KiB / 1.75 MiB per step). HF eager, DynamicCache;
+    prefill and decode overheads reported apart."""
+    import torch
+    from transformers import DynamicCache
+
+    from paper_2605_11093_b200 import (DrainConfig, NullSink, PolicyConfig,
+                                       RingConfig, StepRequest)
+    from paper_2605_11093_b200.hookpoint import Observer
+    from paper_2605_11093_b200.integrations import attach_llama, detach, llama_registry
+    B, T, D = args.c2_batch, args.c2_prefill, args.c2_decode
+    cfg = model.config
+    inner = model.model
+    stream = torch.cuda.current_stream(dev)
+    g = torch.Generator(device=dev).manual_seed(11)
+    ids = torch.randint(0, cfg.vocab_size, (B, T), device=dev, generator=g)
+    dec_ids = torch.randint(0, cfg.vocab_size, (D, B, 1), device=dev, generator=g)
+    pre_reqs = [StepRequest(i, i, f"p{i}", T, 0) for i in range(B)]
+    dec_reqs = [[StepRequest(i, i, f"p{i}", 1, T + d) for i in range(B)] for d in range(D)]
+
+    def run(obs):
+        cache = DynamicCache(config=cfg)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize(dev)
+        with torch.inference_mode():
+            ev[0].record(stream)
+            if obs is not None:
+                obs.begin_step(pre_reqs, 0)
+            inner(input_ids=ids, past_key_values=cache, use_cache=True)
+            if obs is not None:
+                obs.end_step(stream)
+            ev[1].record(stream)
+            for d in range(D):
+                if obs is not None:
+                    obs.begin_step(dec_reqs[d], 1 + d)
+                inner(input_ids=dec_ids[d], past_key_values=cache, use_cache=True)
+                if obs is not None:
+                    obs.end_step(stream)
+            ev[2].record(stream)
+        ev[2].synchronize()
+        del cache
+        return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]) / D
+
+    run(None)                                     # warm-up (allocator, kernels)
+    pre0, dec0 = run(None)
+    out = {"workload": f"llama3-8b {B}x{T} prefill + {D} decode steps x {B} tokens, "
+                       "HF eager (sdpa), DynamicCache",
+           "no_capture": {"prefill_ms": pre0, "decode_step_ms": dec0}}
+    for label, sites in (("resid", ("resid_post",)), ("resid_mlp", ("mlp_act", "resid_post"))):
+        reg = llama_registry(cfg, sites)
+        sink = NullSink()
+        obs = Observer(reg, ring=RingConfig(args.model_ring_mib << 20, 4096),
+                       drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
+                                         max_wait=1e-4, staging_buffer_size=128 << 20,
+                                         staging_buffer_count=args.pinned_buffers,
+                                         mode=args.staging, stage_threads=4,
+                                         page_out=args.page_out, split_oversize=True),
+                       policy=PolicyConfig(), sink=sink, device=dev.index, max_batch=B,
+                       max_tokens=T)
+        obs.exporter.copy_payloads = False
+        obs.start()
+        handles = attach_llama(model, obs, sites)
+        n0 = obs.launches
+        pre, dec = run(obs)
+        launches = obs.launches - n0
+        t_tail = time.perf_counter()
+        obs.flush(600)
+        t_tail = time.perf_counter() - t_tail
+        st = obs.ring.state()
+        obs.check_device()
+        detach(handles)
+        obs.close()
+        prefill_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
+        decode_bytes = sum(reg.slice_bytes(h, 1) for h in reg.enabled_ids()) * B
+        out[label] = {"prefill_ms": pre, "prefill_overhead_pct": (pre - pre0) / pre0 * 100,
+                      "decode_step_ms": dec,
+                      "decode_overhead_pct": (dec - dec0) / dec0 * 100,
+                      "prefill_bytes": prefill_bytes, "decode_step_bytes": decode_bytes,
+                      "largest_capture_bytes": max(reg.slice_bytes(h, T) for h in
+                                                   reg.enabled_ids()) * B,
+                      "capture_launches": launches, "records": sink.records_written,
+                      "bytes_exported": sink.bytes_written,
+                      "stall_events": st.stall_events, "export_tail_s": t_tail}
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -634,22 +777,104 @@ def reference_sample(layers: int, B: int, T: int):
     return kind, total, time.perf_counter() - t0
 
 
+def host_info(pin_cpu=None) -> dict:
+    """CPU model, core counts and the NUMA node of the timing thread
+    (BASELINE.md §3)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    cpu = pin_cpu if pin_cpu is not None else os.sched_getaffinity(0).__iter__().__next__()
+    node = None
+    base = Path(f"/sys/devices/system/cpu/cpu{cpu}")
+    if base.exists():
+        nodes = [p.name for p in base.iterdir() if p.name.startswith("node")]
+        node = int(nodes[0][4:]) if nodes else None
+    n_nodes = len([p for p in Path("/sys/devices/system/node").glob("node[0-9]*")]) \
+        if Path("/sys/devices/system/node").exists() else None
+    return {"cpu_model": model, "cpu_count": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)), "pinned_cpu": cpu,
+            "numa_node": node, "numa_nodes": n_nodes}
+
+
+def run_threaded_sample(B, T):
+    """The reference's real-thread runner (wallclock.py:51-203: producer,
+    drain, stage and sink threads under one Condition) on 2 layers of the
+    workload: GB/s = record payload bytes / wall time. Its producer also
+    generates the synthetic content (workload.py:236 batch_payload, Philox);
+    that generation is timed separately and reported beside it."""
+    if _reference_module() != "reference":
+        return None
+    from tapflow.exporter import DrainConfig
+    from tapflow.hooks import DType, HookSpec
+    from tapflow.policy import PolicyConfig
+    from tapflow.rings import RingConfig
+    from tapflow.wallclock import run_threaded
+    from tapflow.workload import (WorkloadSpec, batch_payload, build_requests,
+                                  build_schedule)
+    from tapflow.hooks import install_hooks
+    bf16 = DType.of("bf16")
+    specs = [HookSpec("mlp_act", ("tokens", FFN), bf16, per_layer=True),
+             HookSpec("resid_post", ("tokens", "hidden"), bf16, per_layer=True)]
+    wl = WorkloadSpec(layers=2, hidden=HIDDEN, batch=B, prefill_tokens=T,
+                      decode_steps=1, prefill_compute_time=1e-3,
+                      decode_compute_time=1e-3)
+    step_max = B * T * (HIDDEN + FFN) * 2
+    drain = DrainConfig(min_ready_entries=1, staging_buffer_size=B * T * FFN * 2,
+                        staging_buffer_count=2)
+    t0 = time.perf_counter()
+    res = run_threaded(wl, specs, PolicyConfig(), drain=drain,
+                       ring=RingConfig((2 * step_max + 15) // 16 * 16, 1024))
+    wall = time.perf_counter() - t0
+    nbytes = sum(len(r.payload) for r in res.records)
+    reg = install_hooks(wl.model, specs)
+    sched = build_schedule(wl, build_requests(wl, 0))
+    t1 = time.perf_counter()
+    for step in sched:
+        for hid in reg.enabled_ids():
+            batch_payload(0, reg.hook(hid), step.batch, step.step_seq, step.tokens,
+                          reg.hidden_extent)
+    gen = time.perf_counter() - t1
+    return {"value": nbytes / wall / 1e9, "unit": UNIT, "threads": 4,
+            "wall_s": wall, "bytes": nbytes,
+            "content_generation_s": gen,
+            "value_excluding_generation": nbytes / max(1e-9, wall - gen) / 1e9,
+            "sample": f"run_threaded, 2 layers x (resid_post+mlp_act), {B}x{T} "
+                      "prefill + 1 decode step, NullSink; 4 GIL-bound threads"}
+
+
 def cpu_baseline(B, T, budget_s=12.0):
     cores = 1
     kind, total, dt, n = None, 0, 0.0, 0
-    while dt < budget_s and n < 8:
-        kind, b, t = reference_sample(2, B, T)
-        total += b
-        dt += t
-        n += 1
+    # pin the timing thread to one core (the reference is GIL-bound, 1 core)
+    prev = os.sched_getaffinity(0)
+    cpu = sorted(prev)[0]
+    os.sched_setaffinity(0, {cpu})
+    try:
+        host = host_info(cpu)
+        while dt < budget_s and n < 8:
+            kind, b, t = reference_sample(2, B, T)
+            total += b
+            dt += t
+            n += 1
+    finally:
+        os.sched_setaffinity(0, prev)
+    try:
+        threaded = run_threaded_sample(B, T)
+    except Exception as exc:  # report, never fail the bench on the baseline
+        threaded = {"error": repr(exc)[:200]}
     return {"value": total / dt / 1e9 if dt else None, "unit": UNIT,
             "cores": cores, "kind": kind,
             "sample": f"{n} samples x (2 layers x resid_post+mlp_act, "
                       f"{B}x{T} tokens, bf16) = {total / GiB:.2f} GiB "
                       f"through capture()+ExportPipeline->NullSink, "
-                      f"single-threaded Python (GIL), {dt:.1f}s",
-            "host": {"cpu_count": os.cpu_count(),
-                     "affinity": len(os.sched_getaffinity(0))}}
+                      f"single-threaded Python (GIL) pinned to CPU {cpu}, {dt:.1f}s",
+            "host": host,
+            "run_threaded": threaded}
 
 
 def run_reference(args, dist):
@@ -728,7 +953,11 @@ def main():
                "h2d_bytes_per_step": e["h2d_per_step"],
                "d2h_bytes_per_step": e["d2h_per_step"],
                "steps": e["steps"], "records": e["records"]}
-    model = leg_model(args, dist, dev) if "model" in legs else None
+    llama = build_model(dev) if ("model" in legs or "c2" in legs) else None
+    model = leg_model(args, dist, dev, llama) if "model" in legs else None
+    c2 = leg_c2(args, dist, dev, llama) if "c2" in legs else None
+    del llama
+    torch.cuda.empty_cache()
     if model:
         for mode in model:
             for key in ("resid", "resid_mlp"):
@@ -771,6 +1000,13 @@ def main():
                          "avg_launch_us_event_pair_each": avg_ms_events * 1e3,
                          "avg_launch_us_in_timed_region": v["timed_kernel_avg_us"],
                          "per_kind_us_event_pair_each": v["per_kind_us"],
+                         "per_kind": {k: {"avg_launch_us": d["avg_launch_us"],
+                                          "achieved": 2.0 * d["bytes_per_launch"]
+                                          / (d["avg_launch_us"] * 1e-6) / 1e9,
+                                          "frac": 2.0 * d["bytes_per_launch"]
+                                          / (d["avg_launch_us"] * 1e-6) / 1e9 / peak,
+                                          "bytes_per_launch": d["bytes_per_launch"]}
+                                      for k, d in v["graph_kind_us"].items()},
                          "algorithmic_bytes_per_launch": avg_alg,
                          "note": "one 64-capture step (resid 32 MiB + mlp 112 MiB "
                                  "per layer) replayed as a CUDA graph (as in the "
@@ -785,6 +1021,7 @@ def main():
                                  "peak_kind": "measured pinned cudaMemcpyAsync D2H 256 MiB best of 10",
                                  "end_to_end_frac": value / dist.world / pcie_peak},
             "overhead": model,
+            "c2_prefill_decode": c2,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pcie_bidirectional": bidir,

@@ -265,6 +265,11 @@ typedef struct tf_drain_config {           /* exporter.py:35-51 */
   uint32_t stage_queue_slots;              /* exporter.py:32 (0 = 16) */
   uint32_t stage_threads;                  /* pinned->pageable copy threads (0 = auto) */
   uint32_t page_out;                       /* TF_PAGE_OUT_* */
+  /* 0 (reference behaviour, exporter.py:197-202): a capture larger than one
+     staging buffer is a ConfigError. 1 (extension): it is staged in
+     buffer-sized chunks through ceil(len / staging_buffer_size) buffers of
+     the pool and paged out into one contiguous host allocation. */
+  uint32_t split_oversize;
 } tf_drain_config;
 
 typedef struct tf_stager tf_stager;
@@ -337,7 +342,8 @@ typedef struct tf_paged_batch {
   tf_descriptor* descs;      /* malloc'd, n_entries long */
   uint64_t* starts;          /* malloc'd, n_entries long */
   int32_t pinned_buffer;     /* pool index under TF_PAGE_OUT_HANDOFF, else -1 */
-  uint32_t _pad;
+  uint32_t oversize;         /* 1: payload is a one-off allocation of a split
+                                (chunked) capture, freed on return */
 } tf_paged_batch;
 int tf_stager_next(tf_stager* st, double timeout_s, tf_paged_batch* out);
 /* Return a batch obtained from tf_stager_next (payload back to the pool). */

@@ -130,7 +130,8 @@ class CDrainConfig(C.Structure):
                 ("staging_buffer_count", C.c_uint64), ("mode", C.c_uint32),
                 ("mapped_ctas", C.c_uint32), ("numa_node", C.c_int32),
                 ("stage_queue_slots", C.c_uint32),
-                ("stage_threads", C.c_uint32), ("page_out", C.c_uint32)]
+                ("stage_threads", C.c_uint32), ("page_out", C.c_uint32),
+                ("split_oversize", C.c_uint32)]
 
 
 class CBatchInfo(C.Structure):
@@ -157,7 +158,7 @@ class CPagedBatch(C.Structure):
                 ("reason", C.c_uint32), ("bytes_total", C.c_uint64),
                 ("payload", C.c_void_p), ("descs", C.POINTER(CDescriptor)),
                 ("starts", u64p), ("pinned_buffer", C.c_int32),
-                ("_pad", C.c_uint32)]
+                ("oversize", C.c_uint32)]
 
 
 assert C.sizeof(CDescriptor) == 64

@@ -63,10 +63,13 @@ def build(force: bool = False, verbose: bool = False,
     defines = []
     if variant == "variants":  # rejected copy paths (TF_COPY_PATH=tma|stage)
         defines.append("-DTF_COPY_VARIANTS")
-    if variant and variant.startswith("trace"):
-        defines.append("-DTF_TRACE")
-        for part in variant.split("_")[1:]:  # trace_ablN_cM: ablation N, M CTAs/SM
-            if part.startswith("abl"):
+    if variant and variant != "variants":
+        # e.g. trace_ablN_cM (phase stamps, ablation N, M CTAs/SM) or smem0
+        # (no shared-memory speculation) without stamps
+        for part in variant.split("_"):
+            if part == "trace":
+                defines.append("-DTF_TRACE")
+            elif part.startswith("abl"):
                 defines.append(f"-DTF_ABL={int(part[3:])}")
             elif part.startswith("c"):
                 defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")

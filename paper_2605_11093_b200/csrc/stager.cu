@@ -233,6 +233,9 @@ class CopyPool {
 struct Batch {
   uint64_t id = 0;
   uint32_t buf = 0;
+  // a split (oversize) capture: its chunks' pool buffers in order (buf is
+  // the first); empty for an ordinary batch
+  std::vector<uint32_t> chunk_bufs;
   uint32_t reason = 0;
   std::vector<tf_descriptor> descs;
   std::vector<uint64_t> starts;
@@ -395,6 +398,14 @@ static void ready_summary(tf_stager* st, std::vector<tf_descriptor>& tmp, uint32
   *bytes = b;
 }
 
+// Pool buffers the next batch needs: 1, or ceil(len / buffer) for an
+// oversize head capture when splitting is enabled.
+static uint64_t bufs_needed(const tf_stager* st, const tf_descriptor* head) {
+  const uint64_t cap = st->cfg.staging_buffer_size;
+  if (!st->cfg.split_oversize || head->payload_len <= cap) return 1;
+  return (head->payload_len + cap - 1) / cap;
+}
+
 extern "C" int tf_stager_note_publish(tf_stager* st, double now) {
   if (!st) return TF_ERR_VALUE;
   std::lock_guard<std::mutex> g(st->mu);
@@ -434,22 +445,45 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   uint32_t take = 0;
   uint64_t used = 0;
   std::vector<uint64_t> starts;
-  for (uint32_t i = 0; i < n; ++i) {
-    if (used + ready[i].payload_len > cap) {
-      if (take == 0) {
-        tf_set_error("capture of %llu bytes exceeds the staging buffer (%llu bytes)",
-                     (unsigned long long)ready[i].payload_len, (unsigned long long)cap);
-        return TF_ERR_CONFIG;
-      }
-      break;
+  std::vector<uint32_t> chunk_bufs;
+  if (ready[0].payload_len > cap) {
+    // exporter.py:197-202: the reference rejects a capture no buffer can
+    // hold; with split_oversize it is staged alone, in buffer-sized chunks
+    const uint64_t k = bufs_needed(st, &ready[0]);
+    if (!st->cfg.split_oversize || k > st->bufs.size()) {
+      tf_set_error("capture of %llu bytes exceeds the staging buffer (%llu bytes)%s",
+                   (unsigned long long)ready[0].payload_len, (unsigned long long)cap,
+                   st->cfg.split_oversize ? " x the whole pool" : "");
+      return TF_ERR_CONFIG;
     }
-    starts.push_back(used);
-    used += ready[i].payload_len;
-    ++take;
+    if (st->free_bufs.size() < k) {
+      tf_set_error("a split capture needs %llu staging buffers, %zu free",
+                   (unsigned long long)k, st->free_bufs.size());
+      return TF_ERR_STAGING_EXHAUSTED;
+    }
+    for (uint64_t c = 0; c < k; ++c) {
+      chunk_bufs.push_back(st->free_bufs.back());
+      st->free_bufs.pop_back();
+    }
+    starts.push_back(0);
+    used = ready[0].payload_len;
+    take = 1;
+  } else {
+    for (uint32_t i = 0; i < n; ++i) {
+      if (used + ready[i].payload_len > cap) break;
+      starts.push_back(used);
+      used += ready[i].payload_len;
+      ++take;
+    }
   }
-  uint32_t b = st->free_bufs.back();
-  st->free_bufs.pop_back();
-  st->stats.pool_checkouts += 1;
+  uint32_t b;
+  if (chunk_bufs.empty()) {
+    b = st->free_bufs.back();
+    st->free_bufs.pop_back();
+  } else {
+    b = chunk_bufs[0];
+  }
+  st->stats.pool_checkouts += chunk_bufs.empty() ? 1 : chunk_bufs.size();
   uint64_t in_use = st->bufs.size() - st->free_bufs.size();
   if (in_use > st->stats.pool_max_in_use) st->stats.pool_max_in_use = in_use;
 
@@ -457,7 +491,8 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   uint32_t polled = 0;
   rc = tf_ring_poll_ready(st->ring, take, got.data(), &polled);
   if (rc || polled != take) {
-    st->free_bufs.push_back(b);
+    if (chunk_bufs.empty()) st->free_bufs.push_back(b);
+    for (uint32_t c : chunk_bufs) st->free_bufs.push_back(c);
     if (!rc) {
       tf_set_error("ready window shrank under the drain");
       rc = TF_ERR_PROTOCOL;
@@ -467,6 +502,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   Batch* bt = new Batch();
   bt->id = st->next_id++;
   bt->buf = b;
+  bt->chunk_bufs = chunk_bufs;
   bt->reason = reason;
   bt->descs = got;
   bt->starts = starts;
@@ -477,7 +513,47 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   cudaEventRecord(bt->ev0, st->stream);
   uint8_t* host = st->bufs[b];
   const uint8_t* payload = st->ring->payload;
-  if (st->cfg.mode == TF_STAGE_COPY_ENGINE) {
+  if (!chunk_bufs.empty()) {
+    // one oversize capture: chunk c of its (contiguous) ring region into
+    // pool buffer chunk_bufs[c]
+    const uint64_t src = got[0].payload_offset, len = got[0].payload_len;
+    if (st->cfg.mode == TF_STAGE_COPY_ENGINE) {
+      for (size_t c = 0; c < chunk_bufs.size(); ++c) {
+        const uint64_t a = c * cap, l = std::min(cap, len - a);
+        cudaError_t e = cudaMemcpyAsync(st->bufs[chunk_bufs[c]], payload + src + a, l,
+                                        cudaMemcpyDeviceToHost, st->stream);
+        if (e != cudaSuccess) {
+          tf_set_error("D2H issue failed: %s", cudaGetErrorString(e));
+          return TF_ERR_CUDA;
+        }
+      }
+    } else {
+      size_t c = 0;
+      while (c < chunk_bufs.size()) {
+        MapCopyArgs a;
+        a.n = 0;
+        a.prefix[0] = 0;
+        uint64_t bytes = 0;
+        for (; c < chunk_bufs.size() && a.n < kMapMaxEntries; ++c) {
+          const uint64_t o = c * cap, l = std::min(cap, len - o);
+          a.src[a.n] = payload + src + o;
+          a.dst[a.n] = st->bufs[chunk_bufs[c]];
+          a.len[a.n] = l;
+          bytes += l;
+          a.prefix[a.n + 1] = bytes;
+          ++a.n;
+        }
+        int ctas = st->cfg.mapped_ctas ? (int)st->cfg.mapped_ctas : 32;
+        ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctas, (bytes + 65535) / 65536));
+        mapped_copy_kernel<<<ctas, 256, 0, st->stream>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+          tf_set_error("mapped copy launch failed: %s", cudaGetErrorString(e));
+          return TF_ERR_CUDA;
+        }
+      }
+    }
+  } else if (st->cfg.mode == TF_STAGE_COPY_ENGINE) {
     // merge runs that are adjacent in the ring and in the buffer
     uint32_t i = 0;
     while (i < take) {
@@ -601,6 +677,10 @@ extern "C" int tf_stager_batch_buffer(tf_stager* st, uint64_t id, void** host_pt
   std::lock_guard<std::mutex> g(st->mu);
   Batch* b = find_batch(st, id);
   if (!b) return TF_ERR_VALUE;
+  if (!b->chunk_bufs.empty()) {
+    tf_set_error("a split capture has no single staging buffer; use stage_to_pageable");
+    return TF_ERR_PROTOCOL;
+  }
   int rc = wait_transfer(st, b);
   if (rc) return rc;
   *host_ptr = st->bufs[b->buf];
@@ -641,11 +721,30 @@ extern "C" int tf_stager_complete_transfer(tf_stager* st, uint64_t id, double* s
 }
 
 static void retire_batch(tf_stager* st, Batch* b, bool return_buffer = true) {
-  if (return_buffer) st->free_bufs.push_back(b->buf);
+  if (!b->chunk_bufs.empty()) {
+    for (uint32_t c : b->chunk_bufs) st->free_bufs.push_back(c);
+  } else if (return_buffer) {
+    st->free_bufs.push_back(b->buf);
+  }
   st->event_pool.push_back(b->ev0);
   st->event_pool.push_back(b->ev1);
   st->batches.erase(b->id);
   delete b;
+}
+
+// The batch's bytes from its pinned buffer(s) into dst (bytes long).
+static void gather_chunks(tf_stager* st, Batch* b, uint8_t* dst, bool parallel) {
+  const uint64_t cap = st->cfg.staging_buffer_size;
+  if (b->chunk_bufs.empty()) {
+    if (parallel) st->copy_pool.copy(dst, st->bufs[b->buf], b->bytes);
+    else memcpy(dst, st->bufs[b->buf], b->bytes);
+    return;
+  }
+  for (size_t c = 0; c < b->chunk_bufs.size(); ++c) {
+    const uint64_t a = c * cap, l = std::min(cap, b->bytes - a);
+    if (parallel) st->copy_pool.copy(dst + a, st->bufs[b->chunk_bufs[c]], l);
+    else memcpy(dst + a, st->bufs[b->chunk_bufs[c]], l);
+  }
 }
 
 extern "C" int tf_stager_stage_to_pageable(tf_stager* st, uint64_t id, void* dst, uint64_t cap) {
@@ -656,7 +755,7 @@ extern "C" int tf_stager_stage_to_pageable(tf_stager* st, uint64_t id, void* dst
   if (cap < b->bytes || (b->bytes && !dst)) { tf_set_error("pageable destination too small"); return TF_ERR_VALUE; }
   int rc = wait_transfer(st, b);
   if (rc) return rc;
-  if (b->bytes) memcpy(dst, st->bufs[b->buf], b->bytes);
+  if (b->bytes) gather_chunks(st, b, (uint8_t*)dst, false);
   st->pageable_in_flight += b->bytes;
   st->stats.batches_staged += 1;
   retire_batch(st, b);  // buffer returns to the pool before anything downstream
@@ -716,7 +815,7 @@ static void free_paged_batch(tf_stager* st, tf_paged_batch* b, bool to_pool) {
     st->free_bufs.push_back((uint32_t)b->pinned_buffer);
     st->cv.notify_all();
   } else if (b->payload) {
-    if (to_pool) st->paged_pool.push_back((uint8_t*)b->payload);
+    if (to_pool && !b->oversize) st->paged_pool.push_back((uint8_t*)b->payload);
     else free(b->payload);
   }
   b->pinned_buffer = -1;
@@ -746,7 +845,7 @@ static void drain_loop(tf_stager* st) {
                                            : reason_for(st, n, bytes, seen.empty() ? -1.0 : now - seen.front());
     if (reason != TF_REASON_NONE) {
       std::unique_lock<std::mutex> g(st->mu);
-      if (st->free_bufs.empty()) {
+      if (st->free_bufs.size() < (n ? std::min<uint64_t>(bufs_needed(st, &tmp[0]), st->bufs.size()) : 1)) {
         st->stats.staging_exhausted_waits += 1;
         st->cv.wait_for(g, std::chrono::microseconds(200));
       } else {
@@ -833,9 +932,21 @@ static void stage_loop(tf_stager* st) {
         st->cv.notify_all();
         continue;
       }
-      if (st->cfg.page_out == TF_PAGE_OUT_COPY) dst = paged_alloc(st);
+      if (st->cfg.page_out == TF_PAGE_OUT_COPY && b->chunk_bufs.empty()) dst = paged_alloc(st);
     }
-    const bool handoff = st->cfg.page_out == TF_PAGE_OUT_HANDOFF;
+    // a split capture is paged out into one contiguous allocation of its
+    // own (the sink needs its payload in one piece), whatever the mode
+    const bool split = !b->chunk_bufs.empty();
+    if (split) {
+      dst = (uint8_t*)aligned_alloc(4096, (b->bytes + 4095) & ~uint64_t(4095));
+      if (!dst) {
+        tf_set_error("pageable allocation of a split capture (%llu bytes) failed",
+                     (unsigned long long)b->bytes);
+        set_bg_error(st, TF_ERR_ALLOCATION);
+        return;
+      }
+    }
+    const bool handoff = st->cfg.page_out == TF_PAGE_OUT_HANDOFF && !split;
     if (!handoff && !dst) {
       tf_set_error("pageable allocation failed");
       set_bg_error(st, TF_ERR_ALLOCATION);
@@ -843,10 +954,11 @@ static void stage_loop(tf_stager* st) {
     }
     // pinned -> pageable (exporter.py:237-249), NUMA-local, parallel; or
     // zero-copy hand-off of the pinned buffer itself
-    if (!handoff) st->copy_pool.copy(dst, st->bufs[b->buf], b->bytes);
+    if (!handoff) gather_chunks(st, b, dst, true);
     tf_paged_batch pb;
     memset(&pb, 0, sizeof(pb));
     pb.pinned_buffer = handoff ? (int32_t)b->buf : -1;
+    pb.oversize = split ? 1u : 0u;
     if (handoff) dst = st->bufs[b->buf];
     pb.batch_id = b->id;
     pb.n_entries = (uint32_t)b->descs.size();

@@ -60,6 +60,10 @@ class DrainConfig:
     # "discard" = D2H-only measurement
     page_out: str = "copy"
     discard_paged: bool = False   # alias for page_out="discard"
+    # extension: a capture larger than one staging buffer is staged in
+    # buffer-sized chunks through several pool buffers (default False keeps
+    # the reference's ConfigError, exporter.py:197-202)
+    split_oversize: bool = False
 
     @property
     def page_out_mode(self) -> str:
@@ -83,7 +87,7 @@ class DrainConfig:
             self.staging_buffer_size, self.staging_buffer_count,
             STAGING_MODES[self.mode], self.mapped_ctas, self.numa_node,
             self.stage_queue_slots, self.stage_threads,
-            N.TF_PAGE_OUT[self.page_out_mode])
+            N.TF_PAGE_OUT[self.page_out_mode], int(self.split_oversize))
 
 
 class StagingBuffer:

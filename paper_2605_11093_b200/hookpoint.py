@@ -176,6 +176,14 @@ class Observer:
         if layout not in ("batch", "flat"):
             raise ConfigError(f"unknown activation layout {layout!r}")
         flat = layout == "flat"
+        if flat and self.persistent:
+            # fail before any state changes (FIFO, plan) if the recorded
+            # graphs' keep buffers cannot hold this step's rows
+            rows = max(sum(r.tokens for r in batch), rows_total or 0)
+            for kind in ("req", "tok"):
+                buf = self._flat.get(kind)
+                if buf is not None and buf.numel() < rows:
+                    self._flat_buf(kind, rows)   # raises ConfigError
         self.registry.commit_filter()
         if not batch:  # engine warm-up / dummy forwards: nothing to keep
             plan = StepPlan(keep=(), flush_before=False, fifo_entries=(), kept_ids=(),

@@ -1,0 +1,193 @@
+// Fixed cost per capture launch, decomposed (experiment, not product code).
+// A decode-size capture (128 KiB, 8 copy CTAs of 16 KiB) emulated piece by
+// piece on top of a plain 128-bit copy, timed as 32 launches replayed in a
+// CUDA graph with programmatic dependent launch (as the capture kernel runs):
+//   bit 1  prologue: tid 0 loads a 96-B "producer snapshot", threads load
+//          the keep bytes; one barrier before the copy (no speculation)
+//   bit 2  end of each CTA: barrier + fence.acq_rel.gpu (completion order)
+//   bit 4  + each CTA stores a completion byte to mapped host memory
+//   bit 8  + controller CTA: posts a 64-B descriptor to mapped host memory,
+//          waits for every copy CTA's snapshot read (red.add / spin), writes
+//          8 x 96-B snapshot replicas
+//   bit 16 a 256 MiB pinned D2H runs on another stream throughout (PCIe busy,
+//          as while the staging engine drains)
+// build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/exp_fixed scripts/exp_fixed.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
+#include <vector>
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e = (x);                                                       \
+    if (e != cudaSuccess) {                                                    \
+      printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e));         \
+      exit(1);                                                                 \
+    }                                                                          \
+  } while (0)
+
+struct Ctl {
+  uint32_t readers;
+  uint32_t pad[31];
+  uint64_t snap[8][16];
+};
+
+__device__ __forceinline__ uint4 ldnc(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                         int64_t words, const uint8_t* keep, Ctl* ctl,
+                                         uint8_t* host_flags, uint64_t* host_desc, int v) {
+  __shared__ uint64_t s_snap[12];
+  __shared__ uint32_t s_keep;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int tid = threadIdx.x;
+  const bool has_ctl = v & 8;
+  const int cb = has_ctl ? int(blockIdx.x) - 1 : int(blockIdx.x);
+  const int cg = has_ctl ? int(gridDim.x) - 1 : int(gridDim.x);
+  if (v & 1) {
+    if (tid == 0) {
+      const uint64_t* q = ctl->snap[blockIdx.x % 8];
+      for (int i = 0; i < 12; ++i) s_snap[i] = *(volatile const uint64_t*)(q + i);
+    }
+    uint32_t kb = tid < 8 ? keep[tid] : 0u;
+    uint32_t m = __ballot_sync(0xffffffffu, kb != 0);
+    if (tid == 0) s_keep = m;
+    __syncthreads();
+    if (tid == 0 && has_ctl && cb >= 0) atomicAdd(&ctl->readers, 1u);
+  }
+  if (has_ctl && cb < 0) {
+    if (tid < 8) host_desc[tid] = s_snap[tid] + tid;  // early descriptor post
+    if (tid == 0) {
+      while (*(volatile uint32_t*)&ctl->readers < uint32_t(cg)) __nanosleep(32);
+      ctl->readers = 0;
+    }
+    __syncthreads();
+    if (tid < 32)
+      for (int r = 0; r < 8; ++r)
+        if (tid < 12) ctl->snap[r][tid] = s_snap[tid] + 1;
+    return;
+  }
+  const int64_t per = (words + cg - 1) / cg;
+  const int64_t w0 = int64_t(cb) * per, w1 = min(words, w0 + per);
+  for (int64_t i = w0 + tid; i < w1; i += 256 * 4) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * 256 < w1) x[u] = ldnc(src + i + u * 256);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * 256 < w1) dst[i + u * 256] = x[u];
+  }
+  if (v & 2) {
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (v & 4)
+        asm volatile("st.relaxed.sys.global.u8 [%0], %1;" ::"l"(host_flags + cb), "h"((unsigned short)1)
+                     : "memory");
+    }
+  }
+}
+
+int main() {
+  const int n = 32, reps = 9;
+  const size_t bytes = 128 << 10;
+  uint8_t *src, *dst, *keep;
+  Ctl* ctl;
+  CK(cudaMalloc(&src, 4 * bytes));
+  CK(cudaMalloc(&dst, 4 * bytes));
+  CK(cudaMalloc(&keep, 256));
+  CK(cudaMemset(keep, 1, 256));
+  CK(cudaMalloc(&ctl, sizeof(Ctl)));
+  CK(cudaMemset(ctl, 0, sizeof(Ctl)));
+  uint8_t* hflags;
+  uint64_t* hdesc;
+  CK(cudaHostAlloc(&hflags, 4096, cudaHostAllocMapped));
+  CK(cudaHostAlloc(&hdesc, 4096, cudaHostAllocMapped));
+  uint8_t *dflags, *ddesc;
+  CK(cudaHostGetDevicePointer((void**)&dflags, hflags, 0));
+  CK(cudaHostGetDevicePointer((void**)&ddesc, hdesc, 0));
+  // background D2H
+  const size_t bg = 256u << 20;
+  void *bg_d, *bg_h;
+  CK(cudaMalloc(&bg_d, bg));
+  CK(cudaHostAlloc(&bg_h, bg, 0));
+  cudaStream_t s, sb;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+  const int variants[] = {0, 1, 2, 6, 3, 7, 9, 15};
+  for (int busy = 0; busy < 2; ++busy) {
+    std::atomic<bool> stop{false};
+    std::thread th;
+    if (busy) {
+      th = std::thread([&] {
+        cudaSetDevice(0);
+        while (!stop.load()) {
+          cudaMemcpyAsync(bg_h, bg_d, bg, cudaMemcpyDeviceToHost, sb);
+          cudaStreamSynchronize(sb);
+        }
+      });
+      std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    }
+    for (int v : variants) {
+      const int grid = 8 + ((v & 8) ? 1 : 0);
+      cudaGraph_t gr;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      for (int i = 0; i < n; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k, (const uint4*)(src + (i % 4) * bytes),
+                              (uint4*)(dst + (i % 4) * bytes), int64_t(bytes / 16),
+                              (const uint8_t*)keep, ctl, dflags, (uint64_t*)ddesc, v));
+      }
+      CK(cudaStreamEndCapture(s, &gr));
+      cudaGraphExec_t ge;
+      CK(cudaGraphInstantiate(&ge, gr, 0));
+      CK(cudaGraphLaunch(ge, s));
+      CK(cudaStreamSynchronize(s));
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      std::vector<float> t;
+      for (int r = 0; r < reps; ++r) {
+        CK(cudaEventRecord(a, s));
+        CK(cudaGraphLaunch(ge, s));
+        CK(cudaEventRecord(b, s));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        t.push_back(ms * 1e3f / n);
+      }
+      std::sort(t.begin(), t.end());
+      printf("{\"variant\": %d, \"d2h_busy\": %d, \"us_per_launch\": %.3f, \"min\": %.3f}\n", v, busy,
+             t[t.size() / 2], t[0]);
+      fflush(stdout);
+      CK(cudaGraphExecDestroy(ge));
+      CK(cudaGraphDestroy(gr));
+    }
+    if (busy) {
+      stop = true;
+      th.join();
+    }
+  }
+  return 0;
+}

@@ -22,13 +22,17 @@ ap.add_argument("--n", type=int, default=16)
 ap.add_argument("--sizes-mib", default="1,4,16,32,64,112,224")
 ap.add_argument("--sizes-kb", default="", help="overrides --sizes-mib (KiB)")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--row-bytes", type=int, default=0,
+                help="source rows of this many bytes (e.g. 8192 = a Llama resid row); "
+                     "0 = one row per batch element")
+ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--out", default="gpurun_out/sweep.json")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
 torch.cuda.set_device(dev)
 PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6545.9
-B = 8
+B = args.batch
 res = []
 ring = RingPair(RingConfig(payload_capacity=24 << 30, meta_slots=4096), device=0)
 pipe = ExportPipeline(ring, DrainConfig(min_ready_entries=1, min_ready_bytes=1, max_wait=1e-4,
@@ -71,14 +75,15 @@ sizes = [int(x) << 10 for x in args.sizes_kb.split(",")] if args.sizes_kb else \
     [int(x) << 20 for x in args.sizes_mib.split(",")]
 for nbytes in sizes:
     mib = nbytes / 1048576
-    row = nbytes // B
+    row = args.row_bytes or nbytes // B
+    mid = nbytes // B // row
     xs = [torch.empty(nbytes, dtype=torch.uint8, device=dev).random_() for _ in range(min(args.n, 4))]
     assert nbytes % B == 0
     dsts = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(min(args.n, 4))]
     caps = []
     for i in range(args.n):
         x = xs[i % len(xs)]
-        src = RowSource(x.data_ptr(), B, 1, row, row, row, x)
+        src = RowSource(x.data_ptr(), B, mid, row, mid * row, row, x)
         caps.append(capture_args(src, hook_id=i, keep_ptr=keep.data_ptr(), keep_per_outer=True,
                                  step_seq=0, full="wait"))
 
@@ -93,7 +98,7 @@ for nbytes in sizes:
     t_cap = timed_graph(cap_step, args.reps)
     t_copy = timed_graph(copy_step, args.reps)
     ideal = 2 * nbytes / (PEAK * 1e9) * 1e6
-    r = {"mib": mib, "capture_us": t_cap, "torch_copy_us": t_copy, "ideal_us": ideal,
+    r = {"mib": mib, "row_bytes": row, "capture_us": t_cap, "torch_copy_us": t_copy, "ideal_us": ideal,
          "capture_frac": ideal / t_cap, "copy_frac": ideal / t_copy}
     print(json.dumps(r), flush=True)
     res.append(r)

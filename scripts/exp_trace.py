@@ -24,6 +24,7 @@ from paper_2605_11093_b200.hooks import RowSource, capture_args, launch_capture 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--sizes-mib", default="1,8,32,112")
+ap.add_argument("--sizes-kb", default="", help="overrides --sizes-mib (KiB)")
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--rows", type=int, default=1, help="rows per batch element (T)")
 args = ap.parse_args()
@@ -76,8 +77,10 @@ def drain():
     pipe.stop(flush=True)
 
 
-for mib in [int(x) for x in args.sizes_mib.split(",")]:
-    nbytes = mib << 20
+sizes = [int(x) << 10 for x in args.sizes_kb.split(",")] if args.sizes_kb else \
+    [int(x) << 20 for x in args.sizes_mib.split(",")]
+for nbytes in sizes:
+    mib = nbytes / 1048576
     T = args.rows
     row = nbytes // (B * T)
     nsrc = max(1, min(args.n, (1 << 30) // nbytes))
@@ -103,7 +106,7 @@ for mib in [int(x) for x in args.sizes_mib.split(",")]:
     s.synchronize()
     ph, gap = trace(args.n)
     span = e0.elapsed_time(e1) * 1e3 / args.n
-    print(f"{mib:5d} MiB  span/launch {span:7.2f} us | entry spread {ph[0]:6.2f} "
+    print(f"{mib:8.3f} MiB  span/launch {span:7.2f} us | entry spread {ph[0]:6.2f} "
           f"| scan {ph[4]:5.2f} | fastplan {ph[5]:5.2f} | table {ph[6]:5.2f} | offset known {ph[1]:6.2f} | copy done {ph[2]:6.2f} | published {ph[3]:6.2f} "
           f"| gap to next {gap:6.2f} | ideal {2 * nbytes / 6545.9e3:6.2f}", flush=True)
     del g, xs, caps

@@ -58,9 +58,9 @@ def test_struct_layouts_match_header(tmp_path):
         "tf_capture_args": ("CCaptureArgs", ["src", "keep", "step_seq_ptr", "flags",
                                              "max_ctas"]),
         "tf_ring_state": ("CRingState", ["occupancy", "high_watermark", "kernel_ns"]),
-        "tf_drain_config": ("CDrainConfig", ["max_wait", "mode", "page_out"]),
+        "tf_drain_config": ("CDrainConfig", ["max_wait", "mode", "page_out", "split_oversize"]),
         "tf_stager_stats": ("CStagerStats", ["transfer_seconds", "pool_free"]),
-        "tf_paged_batch": ("CPagedBatch", ["payload", "starts", "pinned_buffer"]),
+        "tf_paged_batch": ("CPagedBatch", ["payload", "starts", "pinned_buffer", "oversize"]),
         "tf_capture_result": ("CCaptureResult", ["status", "desc"]),
         "tf_ring_config": ("CRingConfig", ["high_watermark", "wait_timeout_ns"]),
         "tf_batch_info": ("CBatchInfo", ["bytes_total", "reason"]),

@@ -423,10 +423,11 @@ def test_persistent_flat_buffers_never_move():
     obs = Observer(reg, ring=RingConfig(1 << 20, 16), sink=Collect(), max_batch=4,
                    flat_rows=16, persistent=True)
     ptr = obs._flat["req"].data_ptr()
+    cap = obs._flat["req"].numel()       # flat_rows, at least max_batch x 64
     obs.begin_step([StepRequest(1, 0, "a", 16, 0)], 0, layout="flat")
     obs.end_step()
     with pytest.raises(ConfigError):
         obs.begin_step([StepRequest(1, 0, "a", 16, 16), StepRequest(2, 1, "b", 1, 0)],
-                       1, layout="flat", rows_total=17)
+                       1, layout="flat", rows_total=cap + 1)
     assert obs._flat["req"].data_ptr() == ptr
     obs.close()
