@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--seq", type=int, default=512)
     p.add_argument("--staging", default="copy-engine",
                    choices=["copy-engine", "mapped"])
-    p.add_argument("--legs", default="value,e2e,model,c2,cpu")
+    p.add_argument("--legs", default="value,e2e,model,c2,gpt2,cpu")
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--page-out", default="handoff",
                    choices=["copy", "handoff"],
@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--c2-decode", type=int, default=128)
     p.add_argument("--model-ring-mib", type=int, default=2048,
                    help="payload ring of the model (overhead) leg")
+    p.add_argument("--replicas-per-gpu", type=int, default=1,
+                   help="independent replicas per GPU (torchrun --nproc-per-node "
+                        "gpus x replicas); value leg only")
     p.add_argument("--profile", action="store_true",
                    help="value leg only, short; for ncu launch lists")
     return p.parse_args()
@@ -72,16 +75,33 @@ def parse():
 # ---------------------------------------------------------------------------
 # distributed plumbing (replicas: barrier + max-over-ranks timing only)
 # ---------------------------------------------------------------------------
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line stays the only stdout line)."""
+    print(f"[bench +{time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 class Dist:
-    def __init__(self) -> None:
+    """Ranks are replicas. ``replicas_per_gpu`` > 1 (``--replicas-per-gpu``,
+    launched with torchrun --nproc-per-node gpus x replicas) places that many
+    independent replicas -- each its own ring pair, staging engine and pinned
+    pool -- on every GPU; their barrier and reductions then use gloo (NCCL
+    rejects two ranks on one device). The data path has no collective."""
+
+    def __init__(self, replicas_per_gpu: int = 1) -> None:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.replicas = max(1, replicas_per_gpu)
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.local = self.local_rank // self.replicas   # the device index
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch.distributed as dist
-            backend = "nccl" if _cuda_ok() else "gloo"
-            dist.init_process_group(backend)
+            self.backend = "nccl" if _cuda_ok() and self.replicas == 1 else "gloo"
+            dist.init_process_group(self.backend)
             self.pg = dist
 
     def barrier(self) -> None:
@@ -92,7 +112,7 @@ class Dist:
         if not self.pg:
             return list(values)
         import torch
-        dev = f"cuda:{self.local}" if _cuda_ok() else "cpu"
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
         t = torch.tensor(list(values), dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=getattr(self.pg.ReduceOp, op.upper()))
         return t.tolist()
@@ -556,6 +576,7 @@ def leg_model(args, dist, dev, model):
             cases.append(("resid_mlp_best_effort", ("mlp_act", "resid_post"),
                           PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT)))
         for label, sites, policy in cases:
+            log(f"model {mode} {label} (base {base:.1f} ms)")
             reg = llama_registry(cfg, sites)
             step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
             sink = NullSink()
@@ -663,8 +684,10 @@ def leg_c2(args, dist, dev, model):
         del cache
         return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]) / D
 
+    log("c2 warm-up")
     run(None)                                     # warm-up (allocator, kernels)
     pre0, dec0 = run(None)
+    log(f"c2 base prefill {pre0:.1f} ms, decode step {dec0:.2f} ms")
     out = {"workload": f"llama3-8b {B}x{T} prefill + {D} decode steps x {B} tokens, "
                        "HF eager (sdpa), DynamicCache",
            "no_capture": {"prefill_ms": pre0, "decode_step_ms": dec0}}
@@ -681,6 +704,7 @@ def leg_c2(args, dist, dev, model):
                        max_tokens=T)
         obs.exporter.copy_payloads = False
         obs.start()
+        log(f"c2 {label}")
         handles = attach_llama(model, obs, sites)
         n0 = obs.launches
         pre, dec = run(obs)
@@ -703,6 +727,173 @@ def leg_c2(args, dist, dev, model):
                       "capture_launches": launches, "records": sink.records_written,
                       "bytes_exported": sink.bytes_written,
                       "stall_events": st.stall_events, "export_tail_s": t_tail}
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# leg: BASELINE configs[0] -- GPT-2 small, 8 x 128, resid_post at all 12
+# layers; the reference CPU path runs on the same activations
+# ---------------------------------------------------------------------------
+def leg_gpt2(args, dist, dev, reps=20):
+    """Random-init GPT-2 small (fp32, the reference's dtype for this config),
+    ids (8, 128) from torch.Generator().manual_seed(0): inference overhead
+    of all-layer resid_post capture (CUDA graph and eager), and the
+    reference CPU path -- tapflow capture() + ExportPipeline -> sink -- timed
+    on the host over the same 12 block outputs, its records compared with
+    the GPU records by crc32 (bit-exact parity on this config)."""
+    import zlib
+
+    import torch
+    from transformers import GPT2Config, GPT2LMHeadModel
+
+    from paper_2605_11093_b200 import (DrainConfig, ModelSpec, RingConfig,
+                                       StepRequest, install_hooks)
+    from paper_2605_11093_b200.hookpoint import Observer
+    from paper_2605_11093_b200.integrations import attach_gpt2, detach, gpt2_specs
+    B, T = 8, 128
+    torch.manual_seed(0)
+    cfg = GPT2Config()
+    model = GPT2LMHeadModel(cfg).to(dev).eval()
+    ids = torch.randint(0, cfg.vocab_size, (B, T),
+                        generator=torch.Generator().manual_seed(0)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    batch = [StepRequest(i, i, f"p{i}", T, 0) for i in range(B)]
+    reg = install_hooks(ModelSpec(cfg.n_layer, cfg.n_embd), gpt2_specs(cfg, "f32"))
+
+    class Keep:
+        records_written = bytes_written = 0
+
+        def __init__(self):
+            self.crc = {}
+
+        def write(self, recs):
+            for r in recs:
+                self.crc[(r.hook_name, r.request_id, r.step_seq)] = zlib.crc32(r.payload)
+                self.records_written += 1
+                self.bytes_written += len(r.payload)
+
+    @torch.inference_mode()
+    def fwd():
+        model.transformer(input_ids=ids, use_cache=False)
+
+    def graph_of(obs=None):
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            for _ in range(2):
+                fwd()
+        stream.wait_stream(cs)
+        g = torch.cuda.CUDAGraph()
+        if obs is None:
+            with torch.inference_mode(), torch.cuda.graph(g):
+                model.transformer(input_ids=ids, use_cache=False)
+        else:
+            with obs.graph_capture(), torch.inference_mode(), torch.cuda.graph(g):
+                model.transformer(input_ids=ids, use_cache=False)
+        return g
+
+    def timed(step, obs=None, base=0):
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(reps):
+            if obs is not None:
+                obs.begin_step(batch, base + k)
+            step()
+            if obs is not None:
+                obs.end_step(stream)
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    out = {"workload": "gpt2-small-random-init-8x128-resid_post-all-12-layers",
+           "dtype": "f32", "bytes_per_forward": B * T * cfg.n_embd * 4 * cfg.n_layer}
+    for mode in ("graph", "eager"):
+        g0 = graph_of() if mode == "graph" else None
+        step0 = g0.replay if g0 is not None else fwd
+        timed(step0)
+        base = timed(step0)
+        sink = Keep()
+        obs = Observer(reg, ring=RingConfig(512 << 20, 1024), sink=sink, max_batch=B,
+                       device=dev.index,
+                       drain=DrainConfig(min_ready_entries=12, staging_buffer_size=8 << 20,
+                                         staging_buffer_count=8))
+        obs.start()
+        handles = attach_gpt2(model, obs)
+        g1 = graph_of(obs) if mode == "graph" else None
+        step1 = g1.replay if g1 is not None else fwd
+        timed(step1, obs, 0)
+        cap = timed(step1, obs, 1000)
+        obs.flush(120)
+        detach(handles)
+        obs.close()
+        out[mode] = {"no_capture_ms": base, "capture_ms": cap,
+                     "overhead_pct": (cap - base) / base * 100.0,
+                     "records": sink.records_written}
+        gpu_crc = sink.crc
+        del g0, g1
+    # the reference CPU path on the same activations (block outputs of one
+    # forward, copied to the host): capture() + ExportPipeline -> sink
+    acts = {}
+    hs = [blk.register_forward_hook(
+        lambda m, a, o, L=L: acts.__setitem__(L, (o[0] if isinstance(o, tuple) else o)
+                                              .detach().float().cpu().contiguous()))
+        for L, blk in enumerate(model.transformer.h)]
+    fwd()
+    for h in hs:
+        h.remove()
+    if _reference_module() == "reference":
+        from tapflow.exporter import DrainConfig as RDrain
+        from tapflow.exporter import ExportPipeline as RPipe
+        from tapflow.hooks import DeviceCopyEngine, DType, HookSpec
+        from tapflow.hooks import ModelSpec as RModel
+        from tapflow.hooks import TensorView, capture
+        from tapflow.hooks import install_hooks as rinstall
+        from tapflow.records import TensorMeta, TensorMetaFIFO
+        from tapflow.rings import RingConfig as RRing
+        from tapflow.rings import RingPair as RPair
+        f32 = DType.of("f32")
+        rreg = rinstall(RModel(cfg.n_layer, cfg.n_embd),
+                        [HookSpec("resid_post", ("tokens", "hidden"), f32, per_layer=True)])
+        views = [TensorView(acts[L].numpy().tobytes(), (B, T, cfg.n_embd), f32)
+                 for L in range(cfg.n_layer)]
+        ref_crc = {}
+
+        class RSink:
+            def write(self, recs):
+                for r in recs:
+                    ref_crc[(r.hook_name, r.request_id)] = zlib.crc32(r.payload)
+
+        times = []
+        for rep in range(5):  # best of 5 (SURVEY §8(d))
+            ring = RPair(RRing(64 << 20, 256))
+            fifo = TensorMetaFIFO()
+            pipe = RPipe(ring, RDrain(min_ready_entries=1, staging_buffer_size=4 << 20),
+                         DeviceCopyEngine(), fifo, hook_name_of=lambda h: rreg.hook(h).name)
+            sink = RSink()
+            t0 = time.perf_counter()
+            for hid in rreg.enabled_ids():
+                hook = rreg.hook(hid)
+                fifo.push(TensorMeta(hook.name, hook.layer_index, 0, tuple(range(B)),
+                                     tuple((0, T) for _ in range(B)),
+                                     hook.resolve_shape(T, cfg.n_embd), f32))
+                capture(rreg, ring, hid, views[hook.layer_index], (1,) * B, step_seq=0)
+                pipe.flush_sync(sink)
+            times.append(time.perf_counter() - t0)
+        best = min(times)
+        # parity: the GPU records of the last graph step equal the reference's
+        last = max(k[2] for k in gpu_crc)
+        same = sum(1 for (name, rid), c in ref_crc.items()
+                   if gpu_crc.get((name, rid, last)) == c)
+        out["reference_cpu"] = {
+            "kind": "reference", "cores": 1, "ms_per_forward": best * 1e3,
+            "value": out["bytes_per_forward"] / best / 1e9, "unit": UNIT,
+            "sample": "12 x (8,128,768) f32 block outputs of one forward through "
+                      "tapflow capture() + ExportPipeline.flush_sync, best of 5",
+            "records": len(ref_crc), "records_bit_exact_vs_gpu": same,
+            "gpu_vs_reference_speedup_forward": best * 1e3 / out["graph"]["capture_ms"]}
+    del model
     torch.cuda.empty_cache()
     return out
 
@@ -914,7 +1105,8 @@ def config_block(args):
             "seq_len": T, "tokens_per_step": B * T,
             "captures_per_step": 2 * LAYERS,
             "bytes_per_step": B * T * (HIDDEN + FFN) * 2 * LAYERS,
-            "parallelism": f"replicas x{args.gpus} (no collective)",
+            "parallelism": f"replicas x{args.gpus * args.replicas_per_gpu} "
+                           f"({args.replicas_per_gpu} per GPU, no collective)",
             "staging": args.staging, "page_out": args.page_out,
             "pinned_pool": f"{args.pinned_buffers} x 128 MiB",
             "l2": "inputs 4.5 GiB/step >> 126 MB L2 (no flush needed)"}
@@ -923,7 +1115,7 @@ def config_block(args):
 # ---------------------------------------------------------------------------
 def main():
     args = parse()
-    dist = Dist()
+    dist = Dist(args.replicas_per_gpu)
     if args.impl == "reference":
         run_reference(args, dist)
         dist.close()
@@ -933,19 +1125,21 @@ def main():
     dev = torch.device(f"cuda:{dist.local}")
     torch.cuda.set_device(dev)
     legs = set(args.legs.split(","))
-    if args.profile:
+    if args.profile or dist.replicas > 1:
         legs = {"value"}
     d2h = __import__("ctypes").c_double()
     N.check(N.lib().tf_measure_d2h(dev.index, 256 << 20, 10, __import__("ctypes").byref(d2h)))
     pcie_peak = d2h.value
     bidir = measure_bidir(dev)
 
+    log("leg value")
     v = leg_value(args, dist, dev)
     staged, elapsed = dist.reduce([v["staged_bytes"]], "sum")[0], \
         dist.reduce([v["elapsed_s"]], "max")[0]
     value = staged / elapsed / 1e9
     e2e = None
     if "e2e" in legs:
+        log("leg e2e")
         e = leg_e2e(args, dist, dev)
         eb = dist.reduce([e["bytes"]], "sum")[0]
         et = dist.reduce([e["elapsed_s"]], "max")[0]
@@ -953,16 +1147,25 @@ def main():
                "h2d_bytes_per_step": e["h2d_per_step"],
                "d2h_bytes_per_step": e["d2h_per_step"],
                "steps": e["steps"], "records": e["records"]}
+    log("build model")
     llama = build_model(dev) if ("model" in legs or "c2" in legs) else None
+    log("leg model")
     model = leg_model(args, dist, dev, llama) if "model" in legs else None
+    log(f"model: {json.dumps(model)}")
+    log("leg c2")
     c2 = leg_c2(args, dist, dev, llama) if "c2" in legs else None
+    log(f"c2: {json.dumps(c2)}")
     del llama
     torch.cuda.empty_cache()
+    log("leg gpt2")
+    gpt2 = leg_gpt2(args, dist, dev) if "gpt2" in legs else None
+    log(f"gpt2: {json.dumps(gpt2)}")
     if model:
         for mode in model:
             for key in ("resid", "resid_mlp"):
                 model[mode][key]["overhead_pct_max_over_ranks"] = dist.reduce(
                     [model[mode][key]["overhead_pct"]], "max")[0]
+    log("leg cpu")
     cpu = cpu_baseline(args.batch, args.seq) if ("cpu" in legs and dist.world == 1
                                                   and dist.rank == 0) else None
 
@@ -985,7 +1188,8 @@ def main():
         steps = args.steps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": dist.world, "steps": steps, "warmup": args.warmup,
+            "n_gpus": dist.world // dist.replicas, "replicas": dist.world,
+            "steps": steps, "warmup": args.warmup,
             "ms_per_step": elapsed / steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 activations; random-init Llama-3-8B)",
@@ -1019,9 +1223,10 @@ def main():
                                  "peak": pcie_peak, "unit": "GB/s",
                                  "frac": d2h_gbs / pcie_peak if d2h_gbs else None,
                                  "peak_kind": "measured pinned cudaMemcpyAsync D2H 256 MiB best of 10",
-                                 "end_to_end_frac": value / dist.world / pcie_peak},
+                                 "end_to_end_frac": value / (dist.world // dist.replicas) / pcie_peak},
             "overhead": model,
             "c2_prefill_decode": c2,
+            "gpt2_config0": gpt2,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pcie_bidirectional": bidir,

@@ -77,7 +77,8 @@ class Observer:
                  sampler: TokenSampler | None = None,
                  sampled_hooks: frozenset = frozenset(),
                  rank_coords: tuple = (0, 0), wait_timeout: float = 60.0,
-                 flat_rows: int = 0, persistent: bool = False):
+                 flat_rows: int = 0, persistent: bool = False,
+                 debug_row_bytes: dict | None = None):
         t = torch()
         self.registry = registry
         self.policy = policy or PolicyConfig()
@@ -122,6 +123,15 @@ class Observer:
             # first begin_step (profiling, graph capture) see all-zero keeps
             self._layout = "flat"
         self.step_buf = t.zeros(1, dtype=t.int32, device=dev)
+        # debug (parity checks of CUDA-graph engines): every capture also
+        # copies the whole observed tensor into a fixed per-hook buffer, so
+        # the copy is recorded into the same graphs as the capture kernel
+        # and a replay leaves the rows the capture read for comparison
+        self.debug_clone = {}
+        for name, row_bytes in (debug_row_bytes or {}).items():
+            hid = [h.name for h in registry.hooks].index(name)
+            self.debug_clone[hid] = t.zeros(self._flat_rows * row_bytes, dtype=t.uint8,
+                                            device=dev)
         self.token = t.zeros(1, dtype=t.uint8, device=dev)  # custom-op ordering token
         self.index = _register_observer(self)
         self._sc = (None, 0.0, 0, 0)  # policy snapshot, time, bytes planned since, max capture
@@ -422,6 +432,12 @@ class Observer:
             full=self.policy.full_mode)
         launch_capture(self.ring, args, stream)
         self.launches += 1
+        dbg = self.debug_clone.get(hook_id)
+        if dbg is not None:
+            flat_x = x.contiguous().reshape(-1).view(torch().uint8)
+            if flat_x.numel() > dbg.numel():
+                raise ConfigError("debug clone buffer too small")
+            dbg[:flat_x.numel()].copy_(flat_x)
 
 
 class _CompletenessRingView:

@@ -189,6 +189,15 @@ class ObservedWorker(Worker):
         else:
             policy = PolicyConfig(mode=COMPLETENESS)
         self._tf_sink = ListSink() if cfg.get("sink") == "list" else CountingSink()
+        # debug_graph_clone: every capture also copies its whole tensor into
+        # a fixed buffer inside the recorded graphs (Observer.debug_clone);
+        # the rows are read back after each forward as the parity reference
+        dbg_rows = {}
+        if cfg.get("debug_graph_clone"):
+            for h in reg.hooks:
+                width = (hf.intermediate_size if h.name.startswith("mlp_act")
+                         else hf.hidden_size)
+                dbg_rows[h.name] = width * h.dtype.width
         obs = Observer(
             reg, ring=RingConfig(int(cfg["ring_bytes"]), int(cfg["meta_slots"])),
             # reference-sized drain batches (exporter.py:35-51 defaults are
@@ -201,7 +210,8 @@ class ObservedWorker(Worker):
                               staging_buffer_count=int(cfg["staging_buffers"]),
                               page_out="handoff"),
             policy=policy, sink=self._tf_sink, device=self.local_rank,
-            max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True)
+            max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True,
+            debug_row_bytes=dbg_rows)
         # records that outlive the batch (ListSink) must own their bytes
         obs.exporter.copy_payloads = cfg.get("sink") == "list"
         obs.start()
@@ -227,7 +237,25 @@ class ObservedWorker(Worker):
                 return inner_forward(*a, **kw)
             finally:
                 obs.end_step()
+                if dbg_rows:
+                    self._tf_graph_clones()
         runner._model_forward = observed_forward
+        self._tf_dbg_rows = {reg.hooks[h].name: dbg_rows[reg.hooks[h].name]
+                             for h in obs.debug_clone}
+
+    def _tf_graph_clones(self):
+        """Debug: read back the per-hook clone buffers after a forward
+        (eager, piecewise or full graph alike) as (step, hook, rows)."""
+        import torch
+        step = self._tf_step - 1
+        if not self._tf_layouts.get(step):
+            return
+        torch.cuda.current_stream().synchronize()
+        rows = self._tf_rows_total
+        for hid, buf in self._tf_obs.debug_clone.items():
+            name = self._tf_obs.registry.hook(hid).name
+            rb = self._tf_dbg_rows[name]
+            self._tf_clones.append((step, name, buf[:rows * rb].view(rows, rb).cpu()))
 
     def execute_model(self, scheduler_output):
         self._tf_sched = scheduler_output
@@ -258,9 +286,11 @@ class ObservedWorker(Worker):
                     self._tf_req[rid] = ent
                 start = int(ib.num_computed_tokens_cpu[ib.req_id_to_index[rid]])
                 batch.append(StepRequest(ent, ent, "", int(n), start))
+        self._tf_rows_total = int(rows_total)
         # dummy / warm-up forwards get an empty batch: every row dropped
         obs.begin_step(batch, self._tf_step, layout="flat", rows_total=rows_total)
-        if self._tf_cfg.get("debug_clone") or self._tf_cfg.get("sink") == "list":
+        if (self._tf_cfg.get("debug_clone") or self._tf_cfg.get("debug_graph_clone")
+                or self._tf_cfg.get("sink") == "list"):
             self._tf_layouts[self._tf_step] = [(r.request_id, r.tokens) for r in batch]
         self._tf_step += 1
         self._tf_steps += 1

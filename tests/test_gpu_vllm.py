@@ -1,8 +1,10 @@
 """vLLM 0.22 integration (BASELINE configs[3]) on a tiny
 random-init Llama, each mode in its own process (scripts/vllm_check.py):
 eager mode is bit-exact against torch hooks at the same sites; CUDA-graph
-mode (the serving configuration) delivers exactly one record per step,
-hook and scheduled request with the scheduled row count."""
+mode (the serving configuration) is bit-exact against a debug copy of each
+observed tensor recorded into the same graphs beside the capture kernel,
+for every record of every replay, across padded decode batch sizes; both
+deliver exactly one record per step, hook and scheduled request."""
 
 import json
 import os
@@ -30,6 +32,7 @@ def test_vllm_eager_records_bit_exact():
     assert out["ok"], json.dumps(out)
 
 
-def test_vllm_cuda_graph_records_complete():
+def test_vllm_cuda_graph_records_bit_exact():
     out = _run("graph")
     assert out["ok"], json.dumps(out)
+    assert out["bit_exact_checked"] == out["expected"] and out["steps_with_padding"] > 0
