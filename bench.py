@@ -732,6 +732,116 @@ def leg_c2(args, dist, dev, model):
 
 
 # ---------------------------------------------------------------------------
+# leg: overload regime -- prefill-only Llama-3-8B with eager
+# attention, hook filtering (resid -> resid+mlp -> every site incl. the
+# attention patterns) under completeness, and request-granular dropping
+# (best-effort drop-recent) for the all-sites set
+# ---------------------------------------------------------------------------
+def leg_overload(args, dist, dev, steps=12):
+    import torch
+
+    from paper_2605_11093_b200 import (BEST_EFFORT, DROP_RECENT, DrainConfig,
+                                       NullSink, PolicyConfig, RingConfig,
+                                       StepRequest)
+    from paper_2605_11093_b200.hookpoint import Observer
+    from paper_2605_11093_b200.integrations import (attach_llama, detach,
+                                                    llama3_8b_config,
+                                                    llama_registry, random_llama)
+    B, T = args.batch, args.seq
+    cfg = llama3_8b_config(attn="eager")
+    with torch.cuda.device(dev):
+        model = random_llama(cfg, device=str(dev))
+    g = torch.Generator(device=dev).manual_seed(5)
+    ids = torch.randint(0, cfg.vocab_size, (B, T), device=dev, generator=g)
+    stream = torch.cuda.current_stream(dev)
+    batch = [StepRequest(i, i, f"p{i}", T, 0) for i in range(B)]
+
+    def graph_of(obs=None):
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs), torch.inference_mode():
+            for _ in range(2):
+                model.model(input_ids=ids, use_cache=False)
+        stream.wait_stream(cs)
+        gr = torch.cuda.CUDAGraph()
+        ctx = obs.graph_capture() if obs is not None else None
+        if ctx is not None:
+            ctx.__enter__()
+        try:
+            with torch.inference_mode(), torch.cuda.graph(gr):
+                model.model(input_ids=ids, use_cache=False)
+        finally:
+            if ctx is not None:
+                ctx.__exit__(None, None, None)
+        return gr
+
+    def run(gr, obs=None, base=0):
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kept = dropped = 0
+        a.record(stream)
+        for k in range(steps):
+            if obs is not None:
+                plan = obs.begin_step(batch, base + k)
+                kept += len(plan.kept_ids)
+                dropped += len(plan.dropped_ids)
+            gr.replay()
+            if obs is not None:
+                obs.end_step(stream)
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / steps, kept, dropped
+
+    g0 = graph_of()
+    run(g0)
+    base, _, _ = run(g0)
+    del g0
+    all_sites = ("k_slice", "v_slice", "attn_pattern", "attn_out", "mlp_act", "resid_post")
+    cases = [("resid", ("resid_post",), PolicyConfig()),
+             ("resid_mlp", ("mlp_act", "resid_post"), PolicyConfig()),
+             ("all_sites", all_sites, PolicyConfig()),
+             ("all_sites_best_effort", all_sites,
+              PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT))]
+    out = {"workload": f"llama3-8b eager attention, prefill-only {B}x{T}, CUDA graph, "
+                       f"{steps} steps per case, 2 GiB ring",
+           "no_capture_ms": base}
+    for label, sites, policy in cases:
+        log(f"overload {label}")
+        reg = llama_registry(cfg, sites)
+        step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
+        sink = NullSink()
+        obs = Observer(reg, ring=RingConfig(args.model_ring_mib << 20, 4096),
+                       drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
+                                         max_wait=1e-4, staging_buffer_size=128 << 20,
+                                         staging_buffer_count=args.pinned_buffers,
+                                         mode=args.staging, stage_threads=4,
+                                         page_out=args.page_out),
+                       policy=policy, sink=sink, device=dev.index, max_batch=B)
+        obs.exporter.copy_payloads = False
+        obs.start()
+        handles = attach_llama(model, obs, sites)
+        gr = graph_of(obs)
+        run(gr, obs, 0)                  # warm: the ring fills to steady state
+        t, kept, dropped = run(gr, obs, 100)
+        obs.flush(600)
+        st = obs.ring.state()
+        obs.check_device()
+        detach(handles)
+        obs.close()
+        del gr
+        out[label] = {"hooks": len(reg.enabled_ids()), "step_bytes": step_bytes,
+                      "offered_gbs": step_bytes / (base * 1e-3) / 1e9,
+                      "capture_ms": t, "overhead_pct": (t - base) / base * 100.0,
+                      "policy": policy.mode, "kept_request_steps": kept,
+                      "dropped_request_steps": dropped,
+                      "kept_bytes_per_step": step_bytes * kept / max(1, kept + dropped),
+                      "records": sink.records_written, "stall_events": st.stall_events}
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
 # leg: BASELINE configs[0] -- GPT-2 small, 8 x 128, resid_post at all 12
 # layers; the reference CPU path runs on the same activations
 # ---------------------------------------------------------------------------
@@ -1157,6 +1267,11 @@ def main():
     log(f"c2: {json.dumps(c2)}")
     del llama
     torch.cuda.empty_cache()
+    overload = None
+    if "overload" in legs:
+        log("leg overload")
+        overload = leg_overload(args, dist, dev)
+        log(f"overload: {json.dumps(overload)}")
     log("leg gpt2")
     gpt2 = leg_gpt2(args, dist, dev) if "gpt2" in legs else None
     log(f"gpt2: {json.dumps(gpt2)}")
@@ -1227,6 +1342,7 @@ def main():
             "overhead": model,
             "c2_prefill_decode": c2,
             "gpt2_config0": gpt2,
+            "overload": overload,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pcie_bidirectional": bidir,

@@ -353,6 +353,11 @@ int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out);
 int tf_stager_error(tf_stager* st);       /* first background error, 0 if none */
 /* The staging stream (cudaStream_t) the D2H work is issued on. */
 int tf_stager_stream(tf_stager* st, void** stream);
+/* Placement of one replica's staging engine: the CPUs its threads are bound
+   to (the GPU's PCIe-local CPUs, sysfs local_cpulist) and the NUMA node of
+   its pinned pool (-1 unknown). No reference analogue. */
+int tf_stager_placement(tf_stager* st, int32_t* cpus, uint32_t max_cpus,
+                        uint32_t* n_cpus, int32_t* pool_node);
 void tf_free_host(void* p);
 
 /* ---- measurement helpers (bench) ------------------------------------- */
@@ -396,6 +401,9 @@ int tf_sink_open_stream(int fd, uint32_t threads, tf_sink** out);
 int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n_caps);
 int tf_sink_stats(tf_sink* s, uint64_t* records, uint64_t* bytes);
 int tf_sink_flush(tf_sink* s);   /* fsync-free: data handed to the kernel */
+/* zlib.crc32(data, crc) as the sinks compute it (PCLMULQDQ folding, zlib
+   fallback); records.py / SRC/records.py checksum semantics */
+uint32_t tf_sink_crc32(uint32_t crc, const void* data, uint64_t n);
 int tf_sink_close(tf_sink* s);   /* closes the files it opened, not a caller fd */
 
 #ifdef __cplusplus

@@ -208,6 +208,8 @@ _SIGS = [
     ("tf_stager_stats_get", C.c_int, [C.c_void_p, C.POINTER(CStagerStats)]),
     ("tf_stager_error", C.c_int, [C.c_void_p]),
     ("tf_stager_stream", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tf_stager_placement", C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32,
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
     ("tf_free_host", None, [C.c_void_p]),
     ("tf_measure_d2h", C.c_int, [C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_double)]),
     ("tf_monotonic", C.c_double, []),
@@ -217,6 +219,7 @@ _SIGS = [
     ("tf_sink_stats", C.c_int, [C.c_void_p, u64p, u64p]),
     ("tf_sink_flush", C.c_int, [C.c_void_p]),
     ("tf_sink_close", C.c_int, [C.c_void_p]),
+    ("tf_sink_crc32", C.c_uint32, [C.c_uint32, C.c_void_p, C.c_uint64]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

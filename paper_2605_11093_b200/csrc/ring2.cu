@@ -182,6 +182,15 @@ constexpr int kSpecSmemBytes = kSmemSpec * 8 /*warps*/ * kSeg * 16;
 #define TF_CTAS_PER_SM 2
 #endif
 constexpr int kCtasPerSm = TF_CTAS_PER_SM;
+// TF_CONTROLLER_CTA=1 (experiment builds): the round-1 scheme, one extra CTA
+// that posts the descriptor and, after every copy CTA has counted itself
+// into `readers`, commits the producer state. Default 0: no extra CTA; each
+// copy CTA counts itself with an atomic whose old value it inspects only
+// after its copy, and the last CTA to have read the snapshot commits.
+#ifndef TF_CONTROLLER_CTA
+#define TF_CONTROLLER_CTA 0
+#endif
+constexpr int kCtl = TF_CONTROLLER_CTA;
 
 // ---------------------------------------------------------------------------
 // element conversions (bit-exact with oracle/cast_oracle.c)
@@ -503,6 +512,11 @@ __device__ __forceinline__ uint64_t umod64(uint64_t x, uint64_t m) {
   return x % m;
 }
 
+__device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -726,9 +740,9 @@ template <int MODE, int VW, int IN_DT, int OUT_DT>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams P) {
   __shared__ CapShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // CTA 0 is the controller: it posts the descriptor and commits the
-  // producer state while the others copy; copy CTA cb of cg owns the work.
-  const int cb = int(blockIdx.x) - 1, cg = int(gridDim.x) - 1;
+  // Copy CTA cb of cg owns a share of the work. (Controller builds: CTA 0
+  // owns none; it posts the descriptor and commits the producer state.)
+  const int cb = int(blockIdx.x) - kCtl, cg = int(gridDim.x) - kCtl;
   extern __shared__ __align__(16) uint4 spec_smem[];  // COPY/16: kSpecSmemBytes
   const int64_t U = P.units;
   const uint64_t t_entry = tid == 0 ? globaltimer() : 0;
@@ -756,9 +770,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // behind the keep scan (step is consumed only by the publishing CTA).
   SnapRegs sr;
   uint32_t step = 0;
+  uint64_t L_now = 0, mt_now = 0;  // consumer cursors for the next snapshot
   if (tid == 0 && !(TF_ABL & 4)) {
     snap_load(P, sr);
     step = P.step_ptr ? *P.step_ptr : P.step_imm;
+    if (!kCtl) {  // only the committing CTA uses them; any older L is conservative
+      L_now = ld_relaxed_gpu(&P.dcons->L);
+      mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
+    }
   }
   // The keep bytes of a small keep vector are loaded before the speculative
   // segment: memory requests leave the SM roughly in issue order, and the
@@ -893,6 +912,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // ---- 2. reservation: fast path in every CTA, else leader election ----
   // (the leader's reservation runs while the others prefetch)
   bool leader = false, fast = false;
+  uint32_t readers_before = 0;  // thread 0: CTAs that had read the snapshot before this one
   if (tid == 0) {
     if (TF_ABL & 4) {
       fast = true;
@@ -907,11 +927,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       // completion flags: every CTA reports; CTA 0 posts the descriptor now
       sh.flagmode = cg <= kMaxFlagCtas && P.done_flags != nullptr;
       if (sh.flagmode) {
-        red_add_gpu(&P.ctl->readers, 1u);  // snapshot consumed
+        // snapshot consumed (its values fed fast_plan above). The old value
+        // is needed only after the copy, so the round trip is hidden.
+        if (kCtl) red_add_gpu(&P.ctl->readers, 1u);
+        else readers_before = atom_add_relaxed_gpu(&P.ctl->readers, 1u);
         sh.publish = !(P.flags & TF_CAP_DEFER_PUBLISH);  // every CTA reports
         sh.slot_idx = umod64(sh.fast_mh, P.slots);
       }
-      if (blockIdx.x == 0 || !sh.flagmode)
+      // (every CTA builds it: whichever commits needs it; CTA 0 posts it)
+      if (!kCtl || blockIdx.x == 0 || !sh.flagmode)
         fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? uint32_t(cg) : 0u);
     } else {
       sh.flagmode = 0;
@@ -979,10 +1003,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // Controller, fast path: commit the allocator state, the result record and
   // the next snapshot as soon as every CTA has read the current snapshot,
   // while the copy CTAs copy; then leave (it owns no payload).
-  if (sh.flagmode && cb < 0) {
+  if (kCtl && sh.flagmode && cb < 0) {
     if (tid == 0) {
-      const uint64_t L_now = ld_relaxed_gpu(&P.dcons->L);
-      const uint64_t mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
+      L_now = ld_relaxed_gpu(&P.dcons->L);
+      mt_now = ld_relaxed_gpu(&P.dcons->meta_tail);
       uint32_t ns = 32;
       while (ld_acquire_gpu(&P.ctl->readers) < gridDim.x) {
         __nanosleep(ns);
@@ -1233,6 +1257,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #endif
         st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + cb, 1);
       }
+      if (!kCtl && readers_before == uint32_t(cg) - 1) {
+        // the last CTA to read the snapshot: every CTA of this launch holds
+        // its plan, so the producer state, the result record and the next
+        // launch's snapshot can be written (the next launch reads them only
+        // after this grid completes: stream order / griddepcontrol.wait)
+        fast_state(P, sh, out_bytes, n_rows, L_now, mt_now, t_entry);
+        P.ctl->readers = 0;
+        write_snap(P.ctl, sh.next, 0, 1);
+      }
     }
 #ifdef TF_TRACE
     if (tid == 0 && blockIdx.x < kTrCtas) {
@@ -1247,7 +1280,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #endif
     return;
   }
-  uint64_t L_now = 0, mt_now = 0;
   if (tid == 0) {
     // consumer cursors for the next snapshot, loaded while the fence and the
     // done count are in flight (any older L is conservative)
@@ -1952,7 +1984,7 @@ static int launch(const CapParams& P, int grid, cudaStream_t s) {
   // any stream capture)
   constexpr int smem = (MODE == MODE_COPY && VW == 16 && kSmemSpec > 0) ? kSpecSmemBytes : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid + 1);  // + the controller CTA (blockIdx 0)
+  cfg.gridDim = dim3(grid + kCtl);  // (+ the controller CTA in controller builds)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -2056,9 +2088,9 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
     waves = e ? std::max(1, atoi(e)) : 1;
   }
   const uint64_t chunk = uint64_t(chunk_kb) << 10;
-  // (- 1: the controller CTA the launch adds keeps the whole grid resident)
+  // (- kCtl: a controller CTA must not push the grid past one resident wave)
   int grid_bytes = int(std::min<uint64_t>((out_max + chunk - 1) / chunk,
-                                          uint64_t(g_sm_count) * kCtasPerSm * waves - 1));
+                                          uint64_t(g_sm_count) * kCtasPerSm * waves - kCtl));
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
   int grid = std::max(1, std::max(grid_bytes, grid_table));
   if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));

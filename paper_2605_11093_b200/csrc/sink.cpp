@@ -31,6 +31,7 @@
 #include <thread>
 #include <vector>
 
+#include "crc32_fast.h"
 #include "ring2_internal.h"
 
 namespace {
@@ -324,16 +325,7 @@ extern "C" int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n
     Piece& p = pieces[k];
     const Rec& r = recs[p.rec];
     const uint8_t* base = r.cap->payload + r.off_in_cap + p.a;
-    uLong crc = crc32(0L, Z_NULL, 0);
-    uint64_t n = p.b - p.a;
-    const uint8_t* q = base;
-    while (n) {
-      uInt step = uInt(std::min<uint64_t>(n, 1u << 30));
-      crc = crc32(crc, q, step);
-      q += step;
-      n -= step;
-    }
-    p.crc = uint32_t(crc);
+    p.crc = tf_crc32_fast(0u, base, size_t(p.b - p.a));
     if (!s->stream && p.b > p.a) {
       int rc = pwrite_all(s->fd_bin, base, size_t(p.b - p.a), r.file_off + p.a);
       if (rc) err = rc;
@@ -395,6 +387,12 @@ extern "C" int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n
   s->records += recs.size();
   s->bytes += total;
   return TF_OK;
+}
+
+// zlib.crc32(data, crc) through the sinks' PCLMULQDQ path (tests compare it
+// with zlib on random buffers)
+extern "C" uint32_t tf_sink_crc32(uint32_t crc, const void* p, uint64_t n) {
+  return tf_crc32_fast(crc, static_cast<const uint8_t*>(p), size_t(n));
 }
 
 extern "C" int tf_sink_stats(tf_sink* s, uint64_t* records, uint64_t* bytes) {

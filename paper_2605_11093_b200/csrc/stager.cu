@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <pthread.h>
 #include <sched.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -786,6 +788,27 @@ extern "C" int tf_stager_error(tf_stager* st) { return st ? st->bg_error.load() 
 extern "C" int tf_stager_stream(tf_stager* st, void** stream) {
   if (!st || !stream) return TF_ERR_VALUE;
   *stream = (void*)st->stream;
+  return TF_OK;
+}
+
+// Placement evidence for replicas: the CPUs the staging
+// threads are bound to (the GPU's PCIe-local CPUs) and the NUMA node that
+// holds the pinned pool's first page (move_pages in query mode).
+extern "C" int tf_stager_placement(tf_stager* st, int32_t* cpus, uint32_t max_cpus,
+                                   uint32_t* n_cpus, int32_t* pool_node) {
+  if (!st) return TF_ERR_VALUE;
+  if (n_cpus) *n_cpus = (uint32_t)st->cpus.size();
+  if (cpus)
+    for (uint32_t i = 0; i < max_cpus && i < st->cpus.size(); ++i) cpus[i] = st->cpus[i];
+  if (pool_node) {
+    *pool_node = -1;
+    if (!st->bufs.empty()) {
+      void* page = st->bufs[0];
+      int status = -1;
+      if (syscall(SYS_move_pages, 0, 1UL, &page, nullptr, &status, 0) == 0 && status >= 0)
+        *pool_node = status;
+    }
+  }
   return TF_OK;
 }
 

@@ -511,6 +511,14 @@ class ExportPipeline:
         N.check(N.lib().tf_stager_stream(self._st, C.byref(p)))
         return int(p.value or 0)
 
+    def placement(self) -> dict:
+        """CPUs the staging threads are bound to and the NUMA node of the
+        pinned pool (replica placement)."""
+        cpus = (C.c_int32 * 1024)()
+        n, node = C.c_uint32(), C.c_int32()
+        N.check(N.lib().tf_stager_placement(self._st, cpus, 1024, C.byref(n), C.byref(node)))
+        return {"cpus": list(cpus[:min(n.value, 1024)]), "pool_numa_node": node.value}
+
     def _check_bg(self) -> None:
         if self._bg_error is not None:
             raise self._bg_error

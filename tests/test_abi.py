@@ -22,7 +22,7 @@ HEADER = ROOT / "include" / "ring2.h"
 def header_functions():
     text = HEADER.read_text()
     return sorted(set(re.findall(
-        r"^\s*(?:int|void|double|const char\*)\s+(tf_\w+)\s*\(", text, re.M)))
+        r"^\s*(?:int|void|double|uint32_t|const char\*)\s+(tf_\w+)\s*\(", text, re.M)))
 
 
 def test_library_loads_and_exports_every_symbol():

@@ -146,3 +146,22 @@ def test_exporter_uses_batch_path_only_for_sinks_that_define_it(tmp_path):
     assert not want(FileSink(tmp_path / "a"))
     with NativeFileSink(tmp_path / "b") as s:
         assert want(s)
+
+
+def test_pclmul_crc32_equals_zlib():
+    """The sinks' CRC-32 (PCLMULQDQ folding, csrc/crc32_fast.h) is zlib.crc32
+    for every length, alignment and running seed."""
+    import ctypes as C
+    import random
+    import zlib
+
+    from paper_2605_11093_b200 import _native as N
+    rng = random.Random(11)
+    buf = rng.randbytes(1 << 20)
+    cbuf = C.create_string_buffer(buf, len(buf))
+    base = C.addressof(cbuf)
+    for n in list(range(0, 300)) + [rng.randrange(0, 1 << 19) for _ in range(300)]:
+        off = rng.randrange(0, 4096)
+        seed = rng.randrange(0, 1 << 32)
+        want = zlib.crc32(buf[off:off + n], seed)
+        assert N.lib().tf_sink_crc32(seed, base + off, n) == want, (n, off)

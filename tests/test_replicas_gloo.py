@@ -14,16 +14,16 @@ import torch.multiprocessing as mp
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, replicas=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
                       RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     sys.path.insert(0, str(ROOT))
     import bench
-    d = bench.Dist()
+    d = bench.Dist(replicas)
     d.barrier()
     s = d.reduce([10.0 * (rank + 1)], "sum")[0]
     m = d.reduce([float(rank + 3)], "max")[0]
-    q.put((rank, s, m))
+    q.put((rank, s, m, d.local, d.backend))
     d.close()
 
 
@@ -38,7 +38,26 @@ def test_dist_reduce_sum_and_max():
         p.join(120)
         assert p.exitcode == 0
     got = sorted(q.get(timeout=5) for _ in range(2))
-    assert got == [(0, 30.0, 4.0), (1, 30.0, 4.0)]
+    assert [g[:3] for g in got] == [(0, 30.0, 4.0), (1, 30.0, 4.0)]
+    assert [g[3] for g in got] == [0, 1]
+
+
+def test_two_replicas_per_gpu_share_the_device_over_gloo():
+    # bench.py --replicas-per-gpu 2: ranks 0 and 1 both drive device 0 and
+    # meet over gloo (NCCL rejects two ranks on one device)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 33500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, 2)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    got = sorted(q.get(timeout=5) for _ in range(2))
+    assert [g[:3] for g in got] == [(0, 30.0, 4.0), (1, 30.0, 4.0)]
+    assert [g[3] for g in got] == [0, 0]
+    assert {g[4] for g in got} == {"gloo"}
 
 
 def test_reference_arm_prints_once_under_torchrun():
