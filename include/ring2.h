@@ -396,6 +396,12 @@ typedef struct tf_capture_meta {
 typedef struct tf_sink tf_sink;
 /* records.ndjson + records.bin in `dir` (appended, like FileSink). */
 int tf_sink_open_dataset(const char* dir, uint32_t threads, tf_sink** out);
+/* flags: TF_SINK_DIRECT writes records.bin with O_DIRECT through aligned
+   bounce buffers (fallocate'd ahead, trimmed at close) where the filesystem
+   supports it, else buffered; tf_sink_is_direct tells which. */
+#define TF_SINK_DIRECT 0x1u
+int tf_sink_open_dataset2(const char* dir, uint32_t threads, uint32_t flags, tf_sink** out);
+int tf_sink_is_direct(tf_sink* s);
 /* u32-LE framed (header, payload) records on an open file descriptor. */
 int tf_sink_open_stream(int fd, uint32_t threads, tf_sink** out);
 int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n_caps);

@@ -215,6 +215,9 @@ _SIGS = [
     ("tf_monotonic", C.c_double, []),
     ("tf_sink_open_dataset", C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     ("tf_sink_open_stream", C.c_int, [C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
+    ("tf_sink_open_dataset2", C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32,
+                                        C.POINTER(C.c_void_p)]),
+    ("tf_sink_is_direct", C.c_int, [C.c_void_p]),
     ("tf_sink_write", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
     ("tf_sink_stats", C.c_int, [C.c_void_p, u64p, u64p]),
     ("tf_sink_flush", C.c_int, [C.c_void_p]),

@@ -228,10 +228,23 @@ constexpr uint64_t kCrcChunk = 4u << 20;  // crc work unit (bytes)
 
 }  // namespace
 
+constexpr uint64_t kDirBlock = 4096;        // O_DIRECT alignment (offset, size, address)
+constexpr uint64_t kDirChunk = 8u << 20;    // aligned write unit per task
+constexpr uint64_t kPrealloc = 1ull << 30;  // fallocate step (non-extending DIO writes)
+
 struct tf_sink {
   bool stream = false;
   int fd_bin = -1, fd_json = -1, fd_stream = -1;
   bool own_fds = false;
+  // O_DIRECT sidecar: the file's last partial block is kept in `carry` and
+  // rewritten (zero-padded) by the next batch; ftruncate at close trims the
+  // padding and the fallocate'd tail.
+  bool direct = false;
+  uint8_t* carry = nullptr;
+  uint8_t* carry_next = nullptr;  // written by the batch's last task, then swapped
+  uint64_t alloc_end = 0;
+  std::vector<uint8_t*> bounce;  // one kDirChunk aligned buffer per task slot
+  std::mutex bounce_mu;
   uint64_t offset = 0;  // sidecar size (dataset) / payload offset counter (stream)
   uint64_t records = 0, bytes = 0;
   Pool* pool = nullptr;
@@ -244,11 +257,27 @@ static unsigned pool_size(uint32_t threads) {
   return n > 1 ? n - 1 : 0;  // the calling thread works too
 }
 
+extern "C" int tf_sink_open_dataset2(const char* dir, uint32_t threads, uint32_t flags,
+                                     tf_sink** out);
+extern "C" int tf_sink_close(tf_sink* s);
+
 extern "C" int tf_sink_open_dataset(const char* dir, uint32_t threads, tf_sink** out) {
+  return tf_sink_open_dataset2(dir, threads, 0, out);
+}
+
+extern "C" int tf_sink_open_dataset2(const char* dir, uint32_t threads, uint32_t flags,
+                                     tf_sink** out) {
   if (!dir || !out) return TF_ERR_VALUE;
   mkdir(dir, 0777);
   std::string d(dir);
-  int fb = ::open((d + "/records.bin").c_str(), O_WRONLY | O_CREAT | O_CLOEXEC, 0644);
+  const std::string bin = d + "/records.bin";
+  int fb = -1;
+  bool direct = false;
+  if (flags & TF_SINK_DIRECT) {
+    fb = ::open(bin.c_str(), O_RDWR | O_CREAT | O_CLOEXEC | O_DIRECT, 0644);
+    direct = fb >= 0;  // EINVAL on filesystems without O_DIRECT (tmpfs): buffered
+  }
+  if (fb < 0) fb = ::open(bin.c_str(), O_WRONLY | O_CREAT | O_CLOEXEC, 0644);
   int fj = ::open((d + "/records.ndjson").c_str(), O_WRONLY | O_CREAT | O_APPEND | O_CLOEXEC, 0644);
   if (fb < 0 || fj < 0) {
     tf_set_error("cannot open dataset files in %s: %s", dir, strerror(errno));
@@ -264,7 +293,96 @@ extern "C" int tf_sink_open_dataset(const char* dir, uint32_t threads, tf_sink**
   s->own_fds = true;
   s->offset = uint64_t(st.st_size);  // append (FileSink opens "ab")
   s->pool = new Pool(pool_size(threads));
+  if (direct) {
+    s->direct = true;
+    s->alloc_end = s->offset;
+    if (posix_memalign(reinterpret_cast<void**>(&s->carry), kDirBlock, kDirBlock) != 0 ||
+        posix_memalign(reinterpret_cast<void**>(&s->carry_next), kDirBlock, kDirBlock) != 0) {
+      tf_sink_close(s);
+      return TF_ERR_ALLOCATION;
+    }
+    memset(s->carry, 0, kDirBlock);
+    const uint64_t tail = s->offset % kDirBlock;  // appending to a partial block
+    if (tail && ::pread(fb, s->carry, kDirBlock, off_t(s->offset - tail)) < ssize_t(tail)) {
+      tf_set_error("cannot read the sidecar's last block: %s", strerror(errno));
+      tf_sink_close(s);
+      return TF_ERR_CONFIG;
+    }
+  }
   *out = s;
+  return TF_OK;
+}
+
+extern "C" int tf_sink_is_direct(tf_sink* s) { return s && s->direct ? 1 : 0; }
+
+// O_DIRECT sidecar write of a batch: file bytes [off0, off1) are the
+// captures' payloads back to back. The aligned span [A, B) is cut into
+// kDirChunk tasks; each fills an aligned bounce buffer (carry prefix,
+// payload bytes, zero pad) and issues one pwrite.
+static int direct_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n_caps,
+                        const std::vector<uint64_t>& cap_off, uint64_t off0, uint64_t off1) {
+  if (off1 == off0) return TF_OK;
+  const uint64_t A = off0 / kDirBlock * kDirBlock;
+  const uint64_t B = (off1 + kDirBlock - 1) / kDirBlock * kDirBlock;
+  if (B > s->alloc_end) {  // keep the writes inside i_size (shared-lock DIO)
+    const uint64_t want = std::max(B, s->alloc_end + kPrealloc);
+    if (fallocate(s->fd_bin, 0, off_t(s->alloc_end), off_t(want - s->alloc_end)) == 0)
+      s->alloc_end = want;
+    else
+      s->alloc_end = B;  // not supported: extending writes
+  }
+  const size_t n_tasks = size_t((B - A + kDirChunk - 1) / kDirChunk);
+  {
+    std::lock_guard<std::mutex> g(s->bounce_mu);
+    const size_t slots = std::min<size_t>(n_tasks, 64);
+    while (s->bounce.size() < slots) {
+      void* p = nullptr;
+      if (posix_memalign(&p, kDirBlock, kDirChunk) != 0) return TF_ERR_ALLOCATION;
+      s->bounce.push_back(static_cast<uint8_t*>(p));
+    }
+  }
+  // fill(dst, [a, b)): file bytes a..b from carry / payloads / zeros
+  auto fill = [&](uint8_t* dst, uint64_t a, uint64_t b) {
+    uint64_t pos = a;
+    if (pos < off0) {  // the carried partial block
+      const uint64_t n = std::min(b, off0) - pos;
+      memcpy(dst, s->carry + (pos - A), size_t(n));
+      pos += n;
+    }
+    // payloads: first capture whose range ends after pos
+    uint32_t c = uint32_t(std::upper_bound(cap_off.begin(), cap_off.begin() + n_caps, pos) -
+                          cap_off.begin());
+    c = c ? c - 1 : 0;
+    while (pos < std::min(b, off1) && c < n_caps) {
+      const uint64_t c0 = cap_off[c], c1 = c0 + caps[c].payload_len;
+      if (pos >= c1) { ++c; continue; }
+      const uint64_t n = std::min(std::min(b, off1), c1) - pos;
+      memcpy(dst + (pos - a), caps[c].payload + (pos - c0), size_t(n));
+      pos += n;
+    }
+    if (pos < b) memset(dst + (pos - a), 0, size_t(b - pos));
+  };
+  std::atomic<int> err{TF_OK};
+  std::atomic<size_t> slot_next{0};
+  // tasks run in waves of at most bounce.size() (one buffer each)
+  const size_t wave = s->bounce.size();
+  for (size_t w0 = 0; w0 < n_tasks; w0 += wave) {
+    const size_t nw = std::min(wave, n_tasks - w0);
+    slot_next = 0;
+    s->pool->run(nw, [&](size_t k) {
+      const size_t t = w0 + k;
+      const uint64_t a = A + uint64_t(t) * kDirChunk, b = std::min(B, a + kDirChunk);
+      uint8_t* buf = s->bounce[slot_next.fetch_add(1)];
+      fill(buf, a, b);
+      int rc = pwrite_all(s->fd_bin, buf, size_t(b - a), a);
+      if (rc) err = rc;
+      if (b == B && off1 % kDirBlock)  // the new partial last block
+        memcpy(s->carry_next, buf + (B - kDirBlock - a), kDirBlock);
+    });
+    if (err.load()) return err.load();
+  }
+  if (off1 % kDirBlock == 0) memset(s->carry_next, 0, kDirBlock);
+  std::swap(s->carry, s->carry_next);
   return TF_OK;
 }
 
@@ -326,12 +444,16 @@ extern "C" int tf_sink_write(tf_sink* s, const tf_capture_meta* caps, uint32_t n
     const Rec& r = recs[p.rec];
     const uint8_t* base = r.cap->payload + r.off_in_cap + p.a;
     p.crc = tf_crc32_fast(0u, base, size_t(p.b - p.a));
-    if (!s->stream && p.b > p.a) {
+    if (!s->stream && !s->direct && p.b > p.a) {
       int rc = pwrite_all(s->fd_bin, base, size_t(p.b - p.a), r.file_off + p.a);
       if (rc) err = rc;
     }
   });
   if (err.load()) return err.load();
+  if (!s->stream && s->direct) {
+    int rc = direct_write(s, caps, n_caps, cap_off, s->offset, end_off);
+    if (rc) return rc;
+  }
   for (size_t k = 0; k < pieces.size(); ++k) {
     Rec& r = recs[pieces[k].rec];
     if (pieces[k].a == 0) r.crc = pieces[k].crc;
@@ -411,6 +533,12 @@ extern "C" int tf_sink_flush(tf_sink* s) {
 extern "C" int tf_sink_close(tf_sink* s) {
   if (!s) return TF_OK;
   delete s->pool;
+  if (s->direct) {  // trim the zero pad and the preallocated tail
+    if (ftruncate(s->fd_bin, off_t(s->offset)) != 0) tf_set_error("ftruncate: %s", strerror(errno));
+    free(s->carry);
+    free(s->carry_next);
+    for (uint8_t* b : s->bounce) free(b);
+  }
   if (s->own_fds) {
     ::close(s->fd_bin);
     ::close(s->fd_json);

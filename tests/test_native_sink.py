@@ -165,3 +165,35 @@ def test_pclmul_crc32_equals_zlib():
         seed = rng.randrange(0, 1 << 32)
         want = zlib.crc32(buf[off:off + n], seed)
         assert N.lib().tf_sink_crc32(seed, base + off, n) == want, (n, off)
+
+
+@pytest.mark.parametrize("where", ["tmp", "repo"])
+def test_direct_io_dataset_equals_buffered(tmp_path, where):
+    """NativeFileSink(direct=True): O_DIRECT sidecar through aligned bounce
+    buffers (partial last block carried between batches, preallocation
+    trimmed on close, append to an existing dataset) writes the same bytes
+    as the buffered native sink and the Python FileSink."""
+    import shutil
+    import tempfile
+    base = tmp_path if where == "tmp" else \
+        __import__("pathlib").Path(tempfile.mkdtemp(dir=os.path.dirname(__file__)))
+    try:
+        rng = random.Random(21)
+        recs = _random_records(rng, 300)
+        big = CaptureRecord(3, "mlp_act[1]", 1, 9, (0, 5), (5, (3 << 20) + 3), U8, (0, 0),
+                            rng.randbytes(5 * ((3 << 20) + 3)))
+        batches = [recs[:1], recs[1:90], [big], recs[90:200], recs[200:]]
+        with FileSink(base / "py") as a:
+            for b in batches:
+                a.write(b)
+        with NativeFileSink(base / "dio", threads=4, direct=True) as d:
+            for b in batches[:3]:
+                d.write(b)
+        with NativeFileSink(base / "dio", threads=3, direct=True) as d:  # reopen: append
+            for b in batches[3:]:
+                d.write(b)
+        for name in ("records.ndjson", "records.bin"):
+            assert (base / "py" / name).read_bytes() == (base / "dio" / name).read_bytes()
+    finally:
+        if where == "repo":
+            shutil.rmtree(base, ignore_errors=True)
