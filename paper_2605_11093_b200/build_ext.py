@@ -71,8 +71,8 @@ def build(force: bool = False, verbose: bool = False,
                 defines.append("-DTF_TRACE")
             elif part.startswith("abl"):
                 defines.append(f"-DTF_ABL={int(part[3:])}")
-            elif part == "ctl":  # round-1 controller-CTA publish scheme (A/B)
-                defines.append("-DTF_CONTROLLER_CTA=1")
+            elif part == "noctl":  # last-reader commit, no controller CTA (A/B)
+                defines.append("-DTF_CONTROLLER_CTA=0")
             elif part.startswith("c"):
                 defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")
             elif part.startswith("u"):

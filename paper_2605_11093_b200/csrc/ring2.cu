@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -182,13 +183,16 @@ constexpr int kSpecSmemBytes = kSmemSpec * 8 /*warps*/ * kSeg * 16;
 #define TF_CTAS_PER_SM 2
 #endif
 constexpr int kCtasPerSm = TF_CTAS_PER_SM;
-// TF_CONTROLLER_CTA=1 (experiment builds): the round-1 scheme, one extra CTA
-// that posts the descriptor and, after every copy CTA has counted itself
-// into `readers`, commits the producer state. Default 0: no extra CTA; each
-// copy CTA counts itself with an atomic whose old value it inspects only
-// after its copy, and the last CTA to have read the snapshot commits.
+// TF_CONTROLLER_CTA=1 (default): one extra CTA posts the descriptor and,
+// after every copy CTA has counted itself into `readers` (a fire-and-forget
+// reduction), commits the producer state while the copy CTAs copy.
+// TF_CONTROLLER_CTA=0 (experiment build "noctl"): no extra CTA; each copy
+// CTA counts itself with an atomic whose old value it inspects after its
+// copy, and the last CTA to have read the snapshot commits. Measured slower
+// on B200 (scripts/exp_fixed.cu variants 15 vs 39: the returning atomic's
+// round trip lands on the critical path; 2.23 vs 2.87 us per 128 KiB launch).
 #ifndef TF_CONTROLLER_CTA
-#define TF_CONTROLLER_CTA 0
+#define TF_CONTROLLER_CTA 1
 #endif
 constexpr int kCtl = TF_CONTROLLER_CTA;
 
@@ -2031,7 +2035,22 @@ static int launch_reduce(const CapParams& P, bool vec, int grid, cudaStream_t s)
              : launch<MODE_REDUCE, 1, IN, TF_F32>(P, grid, s);
 }
 
-static int g_sm_count = 0;
+// SM count of the device (lazy, thread-safe: several producer threads may
+// launch captures on different rings concurrently)
+static std::atomic<int> g_sm_count{0};
+
+// Grid sizing knobs (env, read once, thread-safe magic static)
+struct GridKnobs {
+  int chunk_kb, waves;
+};
+static const GridKnobs& grid_knobs() {
+  static const GridKnobs k = [] {
+    const char* e = getenv("TF_CAP_CHUNK_KB");
+    const char* w = getenv("TF_CAP_WAVES");
+    return GridKnobs{e ? std::max(1, atoi(e)) : 16, w ? std::max(1, atoi(w)) : 1};
+  }();
+  return k;
+}
 
 extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (!r || !a) { tf_set_error("null argument"); return TF_ERR_VALUE; }
@@ -2046,10 +2065,12 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   if (rc) return rc;
   int rcd = set_device(r->device);
   if (rcd) return rcd;
-  if (!g_sm_count) {
-    int dev = r->device, n = 148;
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_sm_count = n;
+  int sm_count = g_sm_count.load(std::memory_order_relaxed);
+  if (!sm_count) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, r->device);
+    g_sm_count.store(n, std::memory_order_relaxed);
+    sm_count = n;
   }
   CapParams P = base_params(r);
   P.src = (const uint8_t*)a->src;
@@ -2080,17 +2101,11 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   // grid: one chunk (default 16 KiB) per CTA up to `waves` x kCtasPerSm
   // CTAs per SM. The leader of a slow-path launch is the first CTA to
   // arrive, so CTAs that become resident later never starve it.
-  static int chunk_kb = -1, waves = -1;
-  if (chunk_kb < 0) {
-    const char* e = getenv("TF_CAP_CHUNK_KB");
-    chunk_kb = e ? std::max(1, atoi(e)) : 16;
-    e = getenv("TF_CAP_WAVES");
-    waves = e ? std::max(1, atoi(e)) : 1;
-  }
+  const int chunk_kb = grid_knobs().chunk_kb, waves = grid_knobs().waves;
   const uint64_t chunk = uint64_t(chunk_kb) << 10;
   // (- kCtl: a controller CTA must not push the grid past one resident wave)
   int grid_bytes = int(std::min<uint64_t>((out_max + chunk - 1) / chunk,
-                                          uint64_t(g_sm_count) * kCtasPerSm * waves - kCtl));
+                                          uint64_t(sm_count) * kCtasPerSm * waves - kCtl));
   int grid_table = a->keep ? int((P.units + kTableMax - 5) / (kTableMax - 4)) : 1;
   int grid = std::max(1, std::max(grid_bytes, grid_table));
   if (a->max_ctas) grid = std::max(grid_table, std::min<int>(grid, (int)a->max_ctas));
@@ -2115,7 +2130,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
         attr2 = true;
       }
       int g = int(std::min<uint64_t>((out_max + (16u << 10) - 1) / (16u << 10),
-                                     uint64_t(g_sm_count) * kStgCtasPerSm));
+                                     uint64_t(sm_count) * kStgCtasPerSm));
       g = std::max(std::max(g, grid_table), 1);
       if (a->max_ctas) g = std::max(grid_table, std::min<int>(g, (int)a->max_ctas));
       capture_stage_kernel<<<g, kStgThreads, 2 * kStgChunk, s>>>(P);
@@ -2133,7 +2148,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
         attr_set = true;
       }
-      int g = int(std::min<uint64_t>((out_max + kTmaTile - 1) / kTmaTile, uint64_t(g_sm_count)));
+      int g = int(std::min<uint64_t>((out_max + kTmaTile - 1) / kTmaTile, uint64_t(sm_count)));
       g = std::max(std::max(g, grid_table), 1);
       if (a->max_ctas) g = std::max(grid_table, std::min<int>(g, (int)a->max_ctas));
       capture_tma_kernel<<<g, kTmaThreads, kTmaSmem, s>>>(P);
@@ -2173,7 +2188,7 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   // reduce: one warp per row; size the grid by rows
   {
     int64_t g = (total_rows + kWarps - 1) / kWarps;
-    int gr = int(std::min<int64_t>(g, int64_t(g_sm_count) * kCtasPerSm));
+    int gr = int(std::min<int64_t>(g, int64_t(sm_count) * kCtasPerSm));
     grid = std::max(std::max(gr, grid_table), 1);
   }
   switch (a->in_dtype) {
@@ -2281,17 +2296,17 @@ static inline uint64_t slot_ready(const tf_ring* r, uint64_t slot) {
 // the driver entry point (the value rides in the command, no host buffer);
 // a pinned-slot cudaMemcpyAsync if stream memory ops are unavailable.
 typedef int (*write64_fn)(void*, unsigned long long, unsigned long long, unsigned int);
-static write64_fn g_write64 = nullptr;
-static int g_write64_probe = 0;
+static std::atomic<write64_fn> g_write64{nullptr};
+static std::atomic<int> g_write64_probe{0};  // double-checked: acquire/release
 static std::mutex g_slot_mu;
 static uint64_t* g_slots = nullptr;
 static uint64_t g_slot_next = 0;
 constexpr uint64_t kSlots = 1u << 16;
 
 int tf_internal_write_u64(void* stream, uint64_t* dev_addr, uint64_t value) {
-  if (!g_write64_probe) {
+  if (!g_write64_probe.load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> g(g_slot_mu);
-    if (!g_write64_probe) {
+    if (!g_write64_probe.load(std::memory_order_relaxed)) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q;
       if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
@@ -2304,14 +2319,15 @@ int tf_internal_write_u64(void* stream, uint64_t* dev_addr, uint64_t value) {
           typedef int (*attr_fn)(int*, int, int);
           ((attr_fn)attr)(&ok, 122 /* CAN_USE_64_BIT_STREAM_MEM_OPS */, dev);
         }
-        if (ok && !getenv("TF_NO_STREAM_MEMOPS")) g_write64 = (write64_fn)fn;
+        if (ok && !getenv("TF_NO_STREAM_MEMOPS"))
+          g_write64.store((write64_fn)fn, std::memory_order_relaxed);
       }
       cudaGetLastError();
-      g_write64_probe = 1;
+      g_write64_probe.store(1, std::memory_order_release);
     }
   }
-  if (g_write64) {
-    int rc = g_write64(stream, (unsigned long long)(uintptr_t)dev_addr, value, 0);
+  if (write64_fn w64 = g_write64.load(std::memory_order_relaxed)) {
+    int rc = w64(stream, (unsigned long long)(uintptr_t)dev_addr, value, 0);
     if (rc != 0) {
       tf_set_error("cuStreamWriteValue64 failed (%d)", rc);
       return TF_ERR_CUDA;
