@@ -95,10 +95,23 @@ class Watch:
         self.th = threading.Thread(target=self.run, daemon=True)
 
     def run(self) -> None:
+        last, still, dumped = None, 0, False
         while not self.stop.wait(self.every):
             try:
-                st = self.obs.ring.state()
                 ex = self.obs.exporter.stats()
+                log(f"watch {self.label} stager: inflight={ex['inflight_batches']} "
+                    f"to_stage={ex['to_stage_batches']} out_q={ex['out_q_batches']} "
+                    f"taken={ex['outstanding_paged']} completion_phase="
+                    f"{ex['completion_phase']} stage_phase={ex['stage_phase']}")
+                still = still + 1 if ex["bytes_drained"] == last else 0
+                last = ex["bytes_drained"]
+                if still >= 2 and not dumped:  # no progress: where is every thread?
+                    import traceback
+                    dumped = True
+                    for tid, frame in sys._current_frames().items():
+                        log(f"watch {self.label}: thread {tid}:\n" +
+                            "".join(traceback.format_stack(frame)[-6:]))
+                st = self.obs.ring.state()
                 log(f"watch {self.label}: occ={st.occupancy} head={st.payload_head} "
                     f"tail={st.payload_tail} meta={st.meta_head}/{st.meta_tail} "
                     f"captures={st.captures_launched} stalls={st.stall_events} "
@@ -792,41 +805,16 @@ def leg_overload(args, dist, dev, steps=12):
     stream = torch.cuda.current_stream(dev)
     batch = [StepRequest(i, i, f"p{i}", T, 0) for i in range(B)]
 
-    def graph_of(obs=None):
-        cs = torch.cuda.Stream(device=dev)
-        cs.wait_stream(stream)
-        with torch.cuda.stream(cs), torch.inference_mode():
-            for _ in range(2):
-                model.model(input_ids=ids, use_cache=False)
-        stream.wait_stream(cs)
-        gr = torch.cuda.CUDAGraph()
-        ctx = obs.graph_capture() if obs is not None else None
-        if ctx is not None:
-            ctx.__enter__()
-        try:
-            with torch.inference_mode(), torch.cuda.graph(gr):
-                model.model(input_ids=ids, use_cache=False)
-        finally:
-            if ctx is not None:
-                ctx.__exit__(None, None, None)
-        return gr
+    # eager mode: HF's eager-attention mask builder copies a host scalar to
+    # the device, which CUDA-graph capture rejects
+    class Eager:
+        @staticmethod
+        @torch.inference_mode()
+        def replay():
+            model.model(input_ids=ids, use_cache=False)
 
-    def run(gr, obs=None, base=0):
-        torch.cuda.synchronize(dev)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        kept = dropped = 0
-        a.record(stream)
-        for k in range(steps):
-            if obs is not None:
-                plan = obs.begin_step(batch, base + k)
-                kept += len(plan.kept_ids)
-                dropped += len(plan.dropped_ids)
-            gr.replay()
-            if obs is not None:
-                obs.end_step(stream)
-        b.record(stream)
-        b.synchronize()
-        return a.elapsed_time(b) / steps, kept, dropped
+    def graph_of(obs=None):
+        return Eager
 
     g0 = graph_of()
     run(g0)
@@ -838,7 +826,7 @@ def leg_overload(args, dist, dev, steps=12):
              ("all_sites", all_sites, PolicyConfig()),
              ("all_sites_best_effort", all_sites,
               PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT))]
-    out = {"workload": f"llama3-8b eager attention, prefill-only {B}x{T}, CUDA graph, "
+    out = {"workload": f"llama3-8b eager attention, prefill-only {B}x{T}, eager launches, "
                        f"{steps} steps per case, 2 GiB ring",
            "no_capture_ms": base}
     for label, sites, policy in cases:

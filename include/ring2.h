@@ -304,6 +304,13 @@ typedef struct tf_stager_stats {
   double last_release_time;
   uint64_t pool_total;
   uint64_t pool_free;
+  /* queue depths and thread phases (diagnostics) */
+  uint64_t inflight_batches;     /* D2H issued, not yet complete */
+  uint64_t to_stage_batches;     /* landed, waiting for page-out */
+  uint64_t out_q_batches;        /* paged out, waiting for the consumer */
+  uint64_t outstanding_paged;    /* taken by the consumer, not yet freed */
+  uint32_t completion_phase;     /* 0 idle, 1 waiting on a D2H event, 2 releasing */
+  uint32_t stage_phase;          /* 0 idle, 1 allocating, 2 copying, 3 waiting for out_q room */
 } tf_stager_stats;
 
 int tf_stager_create(tf_ring* ring, const tf_drain_config* cfg, tf_stager** out);

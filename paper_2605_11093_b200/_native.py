@@ -150,7 +150,10 @@ class CStagerStats(C.Structure):
                 ("staging_exhausted_waits", C.c_uint64),
                 ("first_drain_time", C.c_double),
                 ("last_release_time", C.c_double),
-                ("pool_total", C.c_uint64), ("pool_free", C.c_uint64)]
+                ("pool_total", C.c_uint64), ("pool_free", C.c_uint64),
+                ("inflight_batches", C.c_uint64), ("to_stage_batches", C.c_uint64),
+                ("out_q_batches", C.c_uint64), ("outstanding_paged", C.c_uint64),
+                ("completion_phase", C.c_uint32), ("stage_phase", C.c_uint32)]
 
 
 class CPagedBatch(C.Structure):

@@ -276,7 +276,9 @@ struct tf_stager {
   std::deque<tf_paged_batch> out_q;
   std::vector<uint8_t*> paged_pool;
   uint32_t outstanding_paged = 0;
+  uint64_t outstanding_handoff = 0;  // pinned buffers held by the consumer
   std::atomic<int> bg_error{0};
+  std::atomic<uint32_t> completion_phase{0}, stage_phase{0};  // diagnostics
   std::string bg_errmsg;
   CopyPool copy_pool;
 };
@@ -392,9 +394,20 @@ static uint32_t reason_for(tf_stager* st, uint64_t entries, uint64_t bytes,
   return TF_REASON_NONE;
 }
 
+// The ring's ready descriptors as the host mirror shows them; refresh=true
+// first copies the pending window of the device meta ring (one small D2H on
+// the ring's poll stream). A drain iteration refreshes once and then peeks
+// and polls that same snapshot.
+static int ring_ready(tf_ring* r, uint32_t max, tf_descriptor* out, uint32_t* n, bool consume,
+                      bool refresh) {
+  std::lock_guard<std::mutex> g(r->mu);
+  return tf_internal_poll(r, max, out, n, consume, refresh);
+}
+
 static void ready_summary(tf_stager* st, std::vector<tf_descriptor>& tmp, uint32_t* n, uint64_t* bytes) {
   tmp.resize(st->ring->cfg.meta_slots);
-  tf_ring_peek_ready(st->ring, (uint32_t)tmp.size(), tmp.data(), n);
+  *n = 0;
+  if (ring_ready(st->ring, (uint32_t)tmp.size(), tmp.data(), n, false, true)) *n = 0;
   uint64_t b = 0;
   for (uint32_t i = 0; i < *n; ++i) b += tmp[i].payload_len;
   *bytes = b;
@@ -436,7 +449,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   *out = nullptr;
   std::vector<tf_descriptor> ready(st->ring->cfg.meta_slots);
   uint32_t n = 0;
-  int rc = tf_ring_peek_ready(st->ring, (uint32_t)ready.size(), ready.data(), &n);
+  int rc = ring_ready(st->ring, (uint32_t)ready.size(), ready.data(), &n, false, false);
   if (rc) return rc;
   if (n == 0) return TF_OK;
   if (st->free_bufs.empty()) {
@@ -491,7 +504,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
 
   std::vector<tf_descriptor> got(take);
   uint32_t polled = 0;
-  rc = tf_ring_poll_ready(st->ring, take, got.data(), &polled);
+  rc = ring_ready(st->ring, take, got.data(), &polled, true, false);
   if (rc || polled != take) {
     if (chunk_bufs.empty()) st->free_bufs.push_back(b);
     for (uint32_t c : chunk_bufs) st->free_bufs.push_back(c);
@@ -780,6 +793,12 @@ extern "C" int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out) {
   *out = st->stats;
   out->pool_total = st->bufs.size();
   out->pool_free = st->free_bufs.size();
+  out->inflight_batches = st->inflight.size();
+  out->to_stage_batches = st->to_stage.size();
+  out->out_q_batches = st->out_q.size();
+  out->outstanding_paged = st->outstanding_paged;
+  out->completion_phase = st->completion_phase.load();
+  out->stage_phase = st->stage_phase.load();
   return TF_OK;
 }
 
@@ -836,6 +855,7 @@ static void free_paged_batch(tf_stager* st, tf_paged_batch* b, bool to_pool) {
   if (b->pinned_buffer >= 0) {
     // zero-copy hand-off: the pinned staging buffer goes back to the pool
     st->free_bufs.push_back((uint32_t)b->pinned_buffer);
+    if (st->outstanding_handoff) st->outstanding_handoff -= 1;
     st->cv.notify_all();
   } else if (b->payload) {
     if (to_pool && !b->oversize) st->paged_pool.push_back((uint8_t*)b->payload);
@@ -888,12 +908,14 @@ static void drain_loop(tf_stager* st) {
         }
       }
     }
-    if (did) {
+    // every iteration refreshes the mirror with a small D2H (driver calls):
+    // back off while nothing new arrives (10 -> 160 us), poll at once after
+    // progress or under a flush
+    if (did || st->flush_req.load()) {
       idle = 0;
-    } else if (++idle < 2000) {
-      cpu_relax();
     } else {
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      idle = std::min(idle + 1, 5);
+      std::this_thread::sleep_for(std::chrono::microseconds(5 << idle));
     }
   }
   st->drain_done = true;
@@ -913,7 +935,9 @@ static void completion_loop(tf_stager* st) {
       if (st->inflight.empty()) break;
       b = st->inflight.front();
     }
+    st->completion_phase = 1;
     cudaError_t e = cudaEventSynchronize(b->ev1);
+    st->completion_phase = 2;
     std::unique_lock<std::mutex> g(st->mu);
     if (e != cudaSuccess) {
       tf_set_error("D2H failed: %s", cudaGetErrorString(e));
@@ -930,6 +954,7 @@ static void completion_loop(tf_stager* st) {
     }
     st->inflight.pop_front();
     st->to_stage.push_back(b);
+    st->completion_phase = 0;
     st->cv.notify_all();
   }
   st->completion_done = true;
@@ -941,6 +966,7 @@ static void stage_loop(tf_stager* st) {
   for (;;) {
     Batch* b = nullptr;
     uint8_t* dst = nullptr;
+    bool handoff_ok = false;
     {
       std::unique_lock<std::mutex> g(st->mu);
       st->cv.wait(g, [&] { return !st->to_stage.empty() || st->completion_done.load() || st->bg_error; });
@@ -955,11 +981,23 @@ static void stage_loop(tf_stager* st) {
         st->cv.notify_all();
         continue;
       }
-      if (st->cfg.page_out == TF_PAGE_OUT_COPY && b->chunk_bufs.empty()) dst = paged_alloc(st);
+      // Hand-off keeps a pinned buffer out of the pool until the consumer
+      // frees the batch. The consumer may be Python (needs the GIL), and the
+      // inference thread may block on the device holding the GIL while the
+      // device waits for ring space (completeness): buffers the consumer
+      // holds must never starve the drain. So a batch is handed off only
+      // while at least half the pool stays with the engine; otherwise it is
+      // copied out, and its buffer returns at once.
+      handoff_ok = st->cfg.page_out == TF_PAGE_OUT_HANDOFF &&
+                   2 * (st->outstanding_handoff + 1) <= st->bufs.size();
+      if ((st->cfg.page_out == TF_PAGE_OUT_COPY || !handoff_ok) && b->chunk_bufs.empty())
+        dst = paged_alloc(st);
+      if (handoff_ok && b->chunk_bufs.empty()) st->outstanding_handoff += 1;
     }
     // a split capture is paged out into one contiguous allocation of its
     // own (the sink needs its payload in one piece), whatever the mode
     const bool split = !b->chunk_bufs.empty();
+    st->stage_phase = 1;
     if (split) {
       dst = (uint8_t*)aligned_alloc(4096, (b->bytes + 4095) & ~uint64_t(4095));
       if (!dst) {
@@ -969,7 +1007,7 @@ static void stage_loop(tf_stager* st) {
         return;
       }
     }
-    const bool handoff = st->cfg.page_out == TF_PAGE_OUT_HANDOFF && !split;
+    const bool handoff = handoff_ok && !split;
     if (!handoff && !dst) {
       tf_set_error("pageable allocation failed");
       set_bg_error(st, TF_ERR_ALLOCATION);
@@ -977,6 +1015,7 @@ static void stage_loop(tf_stager* st) {
     }
     // pinned -> pageable (exporter.py:237-249), NUMA-local, parallel; or
     // zero-copy hand-off of the pinned buffer itself
+    st->stage_phase = 2;
     if (!handoff) gather_chunks(st, b, dst, true);
     tf_paged_batch pb;
     memset(&pb, 0, sizeof(pb));
@@ -999,7 +1038,9 @@ static void stage_loop(tf_stager* st) {
       retire_batch(st, b, !handoff);  // copy mode: buffer back before the hand-off
       note_transient(st);
       st->cv.notify_all();
+      st->stage_phase = 3;
       st->cv.wait(g, [&] { return st->out_q.size() < st->cfg.stage_queue_slots || st->stop_req; });
+      st->stage_phase = 0;
       st->out_q.push_back(pb);
       st->cv.notify_all();
     }

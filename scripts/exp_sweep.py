@@ -27,6 +27,9 @@ ap.add_argument("--row-bytes", type=int, default=0,
                      "0 = one row per batch element")
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--out", default="gpurun_out/sweep.json")
+ap.add_argument("--busy-d2h", action="store_true",
+                help="a 256 MiB pinned D2H loops on another stream during the timed "
+                     "replays (PCIe saturated, as while the staging engine drains)")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -48,6 +51,35 @@ def drain():
     pipe.stop(flush=True)
 
 
+class BusyD2H:
+    """Background thread looping a pinned 256 MiB D2H on its own stream."""
+
+    def __init__(self):
+        import threading
+        self.src = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.dst = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        self.st = torch.cuda.Stream()
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        torch.cuda.set_device(dev)
+        while not self.stop.is_set():
+            with torch.cuda.stream(self.st):
+                self.dst.copy_(self.src, non_blocking=True)
+            self.st.synchronize()
+
+    def __enter__(self):
+        self.th.start()
+        import time
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.th.join()
+
+
 def timed_graph(fn, reps):
     with torch.cuda.stream(s):
         fn()  # warm
@@ -60,11 +92,16 @@ def timed_graph(fn, reps):
     for _ in range(reps):
         drain()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        busy = BusyD2H() if args.busy_d2h else None
+        if busy:
+            busy.__enter__()
         with torch.cuda.stream(s):
             e0.record()
             g.replay()
             e1.record()
         s.synchronize()
+        if busy:
+            busy.__exit__()
         out.append(e0.elapsed_time(e1) * 1e3 / args.n)
     del g
     drain()
@@ -98,7 +135,7 @@ for nbytes in sizes:
     t_cap = timed_graph(cap_step, args.reps)
     t_copy = timed_graph(copy_step, args.reps)
     ideal = 2 * nbytes / (PEAK * 1e9) * 1e6
-    r = {"mib": mib, "row_bytes": row, "capture_us": t_cap, "torch_copy_us": t_copy, "ideal_us": ideal,
+    r = {"mib": mib, "row_bytes": row, "busy_d2h": args.busy_d2h, "capture_us": t_cap, "torch_copy_us": t_copy, "ideal_us": ideal,
          "capture_frac": ideal / t_cap, "copy_frac": ideal / t_copy}
     print(json.dumps(r), flush=True)
     res.append(r)

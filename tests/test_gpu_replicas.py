@@ -44,19 +44,24 @@ def _replica(rank, barrier, q):
     obs.start()
     hps = [HookPoint(f"resid[{L}]", obs) for L in range(LAYERS)]
     want = {}
-    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    g = torch.Generator().manual_seed(1000 + rank)
     reqs = [StepRequest(10 * rank + i, i, "p", T, 0) for i in range(B)]
+    # content made on the host and uploaded without a device sync in the
+    # loop (a blocking copy would hold the GIL while the device may wait for
+    # the exporter thread)
+    host = [torch.empty(B, T, H, dtype=torch.int16).random_(-32768, 32767, generator=g)
+            .view(torch.bfloat16).pin_memory() for _ in range(LAYERS * STEPS)]
+    dev = [torch.empty(B, T, H, dtype=torch.bfloat16, device="cuda") for _ in host]
     barrier.wait()  # both replicas capture at the same time
     for step in range(STEPS):
         obs.begin_step(reqs, step)
         for L, hp in enumerate(hps):
-            x = torch.empty(B, T, H, dtype=torch.bfloat16, device="cuda")
-            x.view(torch.int16).random_(-32768, 32767, generator=g)
-            hp(x)
-            host = x.cpu()
+            k = step * LAYERS + L
+            dev[k].copy_(host[k], non_blocking=True)
+            hp(dev[k])
             for i, r in enumerate(reqs):
                 want[(f"resid[{L}]", r.request_id, step)] = zlib.crc32(
-                    host[i].contiguous().view(torch.uint8).numpy().tobytes())
+                    host[k][i].contiguous().view(torch.uint8).numpy().tobytes())
         obs.end_step()
     obs.flush(120)
     place = obs.exporter.placement()
