@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -2422,6 +2423,8 @@ static int refresh_mirror(tf_ring* r, uint64_t count) {
   if (!count) return TF_OK;
   int rc = set_device(r->device);
   if (rc) return rc;
+  RelaxedCaptureMode relaxed;  // may run while another thread records a graph
+  const auto t0 = std::chrono::steady_clock::now();
   const uint64_t first = r->meta_tail % slots;
   const uint64_t n1 = std::min(count, slots - first);
   cudaStream_t s = (cudaStream_t)r->poll_stream;
@@ -2431,7 +2434,12 @@ static int refresh_mirror(tf_ring* r, uint64_t count) {
     CUDA_TRY(cudaMemcpyAsync(r->hmirror, r->dmeta, (count - n1) * kMetaStride,
                              cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  r->refreshes += 1;
+  const uint64_t ns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+      std::chrono::steady_clock::now() - t0).count());
+  r->refreshes.fetch_add(1, std::memory_order_relaxed);
+  r->refresh_ns.fetch_add(ns, std::memory_order_relaxed);
+  if (ns > r->refresh_max_ns.load(std::memory_order_relaxed))
+    r->refresh_max_ns.store(ns, std::memory_order_relaxed);  // caller holds r->mu
   return TF_OK;
 }
 

@@ -21,12 +21,28 @@
 #pragma once
 #include <stdint.h>
 
+#include <atomic>
 #include <deque>
 #include <vector>
 #include <map>
 #include <mutex>
 
+#include <cuda_runtime.h>
+
 #include "ring2_core.h"
+
+// Host threads of the consumer side (poll refreshes, staging threads) make
+// stream-synchronising calls on their own private streams. Under another
+// thread's global-mode CUDA graph capture (torch.cuda.graph's default) those
+// calls would invalidate the capture, so these threads run in relaxed
+// capture mode: nothing they touch is being captured.
+struct RelaxedCaptureMode {
+  cudaStreamCaptureMode prev = cudaStreamCaptureModeRelaxed;
+  RelaxedCaptureMode() { cudaThreadExchangeStreamCaptureMode(&prev); }
+  ~RelaxedCaptureMode() { cudaThreadExchangeStreamCaptureMode(&prev); }
+  RelaxedCaptureMode(const RelaxedCaptureMode&) = delete;
+  RelaxedCaptureMode& operator=(const RelaxedCaptureMode&) = delete;
+};
 
 struct alignas(128) DevConsumer {
   uint64_t L;          // virtual release cursor (ring2_core.h)
@@ -107,7 +123,9 @@ struct tf_ring {
   uint8_t* hmirror = nullptr;
   void* poll_stream = nullptr;
   std::vector<uint32_t> done_base;  // per slot: CTA completions of earlier captures
-  uint64_t refreshes = 0;
+  // mirror refreshes: count, summed and worst wall time (diagnostics; the
+  // small D2H can queue behind staging transfers on the copy engine)
+  std::atomic<uint64_t> refreshes{0}, refresh_ns{0}, refresh_max_ns{0};
   DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
   DevCtl* ctl_host = nullptr;     // pinned, host-mapped snapshot target

@@ -799,6 +799,9 @@ extern "C" int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out) {
   out->outstanding_paged = st->outstanding_paged;
   out->completion_phase = st->completion_phase.load();
   out->stage_phase = st->stage_phase.load();
+  out->meta_refreshes = st->ring->refreshes.load(std::memory_order_relaxed);
+  out->meta_refresh_ns = st->ring->refresh_ns.load(std::memory_order_relaxed);
+  out->meta_refresh_max_ns = st->ring->refresh_max_ns.load(std::memory_order_relaxed);
   return TF_OK;
 }
 
@@ -871,6 +874,7 @@ static void free_paged_batch(tf_stager* st, tf_paged_batch* b, bool to_pool) {
 
 static void drain_loop(tf_stager* st) {
   bind_thread(st->cpus);
+  RelaxedCaptureMode relaxed;  // ring2_internal.h
   cudaSetDevice(st->device);
   std::vector<tf_descriptor> tmp;
   std::deque<double> seen;  // observation times of ready entries (max_wait)
@@ -926,6 +930,7 @@ static void drain_loop(tf_stager* st) {
 // sleeps in the driver), then release its regions and hand it to staging.
 static void completion_loop(tf_stager* st) {
   bind_thread(st->cpus);
+  RelaxedCaptureMode relaxed;  // ring2_internal.h
   cudaSetDevice(st->device);
   for (;;) {
     Batch* b = nullptr;
@@ -963,6 +968,7 @@ static void completion_loop(tf_stager* st) {
 
 static void stage_loop(tf_stager* st) {
   bind_thread(st->cpus);
+  RelaxedCaptureMode relaxed;  // ring2_internal.h
   for (;;) {
     Batch* b = nullptr;
     uint8_t* dst = nullptr;

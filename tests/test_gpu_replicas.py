@@ -21,6 +21,17 @@ LAYERS, B, T, H, STEPS = 4, 4, 64, 1024, 24
 
 
 def _replica(rank, barrier, q):
+    """Child entry: report a failure at once instead of leaving the parent
+    waiting on the queue."""
+    try:
+        _replica_body(rank, barrier, q)
+    except BaseException:
+        import traceback
+        q.put({"rank": rank, "error": traceback.format_exc()})
+        raise
+
+
+def _replica_body(rank, barrier, q):
     sys.path.insert(0, str(ROOT))
     import torch
 
@@ -52,7 +63,7 @@ def _replica(rank, barrier, q):
     host = [torch.empty(B, T, H, dtype=torch.int16).random_(-32768, 32767, generator=g)
             .view(torch.bfloat16).pin_memory() for _ in range(LAYERS * STEPS)]
     dev = [torch.empty(B, T, H, dtype=torch.bfloat16, device="cuda") for _ in host]
-    barrier.wait()  # both replicas capture at the same time
+    barrier.wait(120)  # both replicas capture at the same time
     for step in range(STEPS):
         obs.begin_step(reqs, step)
         for L, hp in enumerate(hps):
@@ -66,11 +77,12 @@ def _replica(rank, barrier, q):
     obs.flush(120)
     place = obs.exporter.placement()
     st = obs.ring.state()
+    released = obs.ring.bytes_released
     obs.close()
     bad = sum(1 for k, c in want.items() if got.get(k) != c)
     q.put({"rank": rank, "records": len(got), "expected": len(want), "mismatch": bad,
            "foreign": sum(1 for k in got if k not in want),
-           "bytes": st.bytes_released, "stalls": st.stall_events, "placement": place,
+           "bytes": released, "stalls": st.stall_events, "placement": place,
            "pid": os.getpid()})
 
 
@@ -99,6 +111,8 @@ def test_two_replicas_on_one_gpu_are_isolated_and_numa_bound():
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=600) for _ in procs), key=lambda d: d["rank"])
+    for r in res:
+        assert "error" not in r, r["error"]
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
