@@ -98,11 +98,16 @@ class Watch:
         last, still, dumped = None, 0, False
         while not self.stop.wait(self.every):
             try:
-                ex = self.obs.exporter.stats()
+                from paper_2605_11093_b200 import _native as N
+                ep = self.obs.exporter
+                ex = ep.stats()
                 log(f"watch {self.label} stager: inflight={ex['inflight_batches']} "
                     f"to_stage={ex['to_stage_batches']} out_q={ex['out_q_batches']} "
                     f"taken={ex['outstanding_paged']} completion_phase="
-                    f"{ex['completion_phase']} stage_phase={ex['stage_phase']}")
+                    f"{ex['completion_phase']} stage_phase={ex['stage_phase']} "
+                    f"pageable={ex['pageable_bytes_in_flight']} "
+                    f"sink_alive={bool(ep._sink_thread and ep._sink_thread.is_alive())} "
+                    f"sink_err={ep._bg_error!r} stager_err={N.lib().tf_stager_error(ep._st)}")
                 still = still + 1 if ex["bytes_drained"] == last else 0
                 last = ex["bytes_drained"]
                 if still >= 2 and not dumped:  # no progress: where is every thread?
@@ -111,7 +116,10 @@ class Watch:
                     for tid, frame in sys._current_frames().items():
                         log(f"watch {self.label}: thread {tid}:\n" +
                             "".join(traceback.format_stack(frame)[-6:]))
-                st = self.obs.ring.state()
+                # without RingPair.sync(): do not wait for the producer stream
+                import ctypes
+                st = N.CRingState()
+                N.lib().tf_ring_get_state(self.obs.ring.handle, ctypes.byref(st))
                 log(f"watch {self.label}: occ={st.occupancy} head={st.payload_head} "
                     f"tail={st.payload_tail} meta={st.meta_head}/{st.meta_tail} "
                     f"captures={st.captures_launched} stalls={st.stall_events} "

@@ -311,10 +311,6 @@ typedef struct tf_stager_stats {
   uint64_t outstanding_paged;    /* taken by the consumer, not yet freed */
   uint32_t completion_phase;     /* 0 idle, 1 waiting on a D2H event, 2 releasing */
   uint32_t stage_phase;          /* 0 idle, 1 allocating, 2 copying, 3 waiting for out_q room */
-  /* host mirror refreshes of the device meta ring (poll latency) */
-  uint64_t meta_refreshes;
-  uint64_t meta_refresh_ns;      /* summed wall time */
-  uint64_t meta_refresh_max_ns;  /* worst single refresh */
 } tf_stager_stats;
 
 int tf_stager_create(tf_ring* ring, const tf_drain_config* cfg, tf_stager** out);

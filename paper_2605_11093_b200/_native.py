@@ -153,9 +153,7 @@ class CStagerStats(C.Structure):
                 ("pool_total", C.c_uint64), ("pool_free", C.c_uint64),
                 ("inflight_batches", C.c_uint64), ("to_stage_batches", C.c_uint64),
                 ("out_q_batches", C.c_uint64), ("outstanding_paged", C.c_uint64),
-                ("completion_phase", C.c_uint32), ("stage_phase", C.c_uint32),
-                ("meta_refreshes", C.c_uint64), ("meta_refresh_ns", C.c_uint64),
-                ("meta_refresh_max_ns", C.c_uint64)]
+                ("completion_phase", C.c_uint32), ("stage_phase", C.c_uint32)]
 
 
 class CPagedBatch(C.Structure):

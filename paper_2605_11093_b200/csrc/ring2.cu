@@ -21,7 +21,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -107,6 +106,14 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -169,12 +176,9 @@ constexpr int kSeg = 32 * kUnroll;  // vector words per warp segment
 #define TF_SMEM_SPEC 2
 #endif
 // COPY with 16-B words: segments 2..(1+kSmemSpec) of each warp are also
-// fetched before the plan, into shared memory with cp.async; after the plan
-// the same slots form a per-warp ring (kSmemSlots = kSmemSpec + 1) that
-// keeps kSmemSpec segments in flight ahead of the one being stored
+// fetched before the plan, into shared memory with cp.async
 constexpr int kSmemSpec = TF_SMEM_SPEC;
-constexpr int kSmemSlots = kSmemSpec > 0 ? kSmemSpec + 1 : 0;
-constexpr int kSpecSmemBytes = kSmemSlots * 8 /*warps*/ * kSeg * 16;
+constexpr int kSpecSmemBytes = kSmemSpec * 8 /*warps*/ * kSeg * 16;
 #ifndef TF_CTAS_PER_SM
 #define TF_CTAS_PER_SM 2
 #endif
@@ -308,15 +312,12 @@ struct CapParams {
   uint8_t* payload;
   uint64_t cap;
   uint64_t slots;
-  uint8_t* meta;              // device meta ring (kMetaStride per slot)
+  uint8_t* meta;              // mapped host memory (descriptors only)
   const DevConsumer* dcons;
   DevCtl* ctl;
   uint64_t timeout_ns;
+  uint8_t* done_flags;        // mapped host memory, kMaxFlagCtas per slot
 };
-
-__device__ __forceinline__ uint32_t* slot_done(const CapParams& P, uint64_t slot) {
-  return reinterpret_cast<uint32_t*>(P.meta + slot * kMetaStride + kMetaDoneOff);
-}
 
 enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
 
@@ -593,7 +594,7 @@ __device__ void fast_desc(const CapParams& P, CapShared& sh, uint64_t bytes, uin
     d.ready_seq = mh;
     d.checksum = tf_desc_checksum(reinterpret_cast<const uint64_t*>(&d));
     sh.slot_idx = umod64(mh, P.slots);
-    sh.slot = reinterpret_cast<uint64_t*>(P.meta + sh.slot_idx * kMetaStride);
+    sh.slot = reinterpret_cast<uint64_t*>(P.meta + sh.slot_idx * TF_DESCRIPTOR_SIZE);
     sh.publish = 1;
     mh += 1;
   }
@@ -666,6 +667,9 @@ __device__ void fast_state(const CapParams& P, CapShared& sh, uint64_t bytes, ui
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys_u8(uint8_t* p, uint8_t v) {
+  asm volatile("st.relaxed.sys.global.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void red_add_gpu(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -706,7 +710,7 @@ __device__ void last_cta_prepare(const CapParams& P, CapShared& sh) {
     const uint64_t seq = c->meta_head;
     d.ready_seq = seq;
     d.checksum = tf_desc_checksum(reinterpret_cast<const uint64_t*>(&d));
-    sh.slot = reinterpret_cast<uint64_t*>(P.meta + (seq % P.slots) * kMetaStride);
+    sh.slot = reinterpret_cast<uint64_t*>(P.meta + (seq % P.slots) * TF_DESCRIPTOR_SIZE);
     sh.publish = 1;
     c->meta_head = seq + 1;
   }
@@ -842,8 +846,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
                         srcn + k * 16);
               }
             }
-            cpa_commit();  // one group per segment (the ring below waits on them in order)
           }
+          cpa_commit();
         }
       }
     }
@@ -925,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     if (fast) {
       sh.status = TF_OK;
       // completion flags: every CTA reports; CTA 0 posts the descriptor now
-      sh.flagmode = cg <= kMaxFlagCtas;
+      sh.flagmode = cg <= kMaxFlagCtas && P.done_flags != nullptr;
       if (sh.flagmode) {
         // snapshot consumed (its values fed fast_plan above). The old value
         // is needed only after the copy, so the round trip is hidden.
@@ -1106,74 +1110,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     const bool smem_ok = VW == 16 && kSmemSpec > 0 && spec_s == s && prefix;
     if (sh.status == TF_OK && s < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
-      if constexpr (VW == 16 && kSmemSpec > 0) {
-        // Streaming ring: slot (t-1) % kSmemSlots holds segment t of this
-        // warp's sequence (segment 0 is in registers); kSmemSpec groups are
-        // in flight ahead of the segment being stored. A slot is refilled one
-        // iteration after it was read (its values have reached the global
-        // store by then).
-        auto seg_smem = [&](int t) {
-          return spec_smem + (size_t(t % kSmemSlots) * kWarps + warp) * kSeg;
-        };
-        auto issue = [&](int t) {  // cp.async segment t (real row map) into its slot
-          const int64_t sn = s_first + int64_t(t) * s_step;
-          if (sn < s_end) {
-            const int64_t jn = qdiv(sn, spr);
-            const int64_t kn0 = (sn - jn * spr) * kSeg;
-            const int64_t kn1 = imin64(kn0 + kSeg, wpr);
-            const uint8_t* srcn = row_src(P, row_of(jn));
-            uint4* slot = seg_smem(t - 1);
+      int it = 0;
+      for (;;) {
+        uint8_t* dst = dst_base + j * P.out_row_bytes;
+#pragma unroll
+        for (int i = 0; i < kUnroll; ++i) {
+          int64_t k = k0 + lane + i * 32;
+          if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
+        }
+        s += s_step;
+        ++it;
+        if (s >= s_end) break;
+        j = qdiv(s, spr);
+        k0 = (s - j * spr) * kSeg;
+        k1 = imin64(k0 + kSeg, wpr);
+        if (smem_ok && it <= kSmemSpec) {
+          if constexpr (VW == 16 && kSmemSpec > 0) {
+            cpa_wait_all();
+            const uint4* slot = spec_smem + (size_t(it - 1) * kWarps + warp) * kSeg;
 #pragma unroll
             for (int i = 0; i < kUnroll; ++i) {
-              int64_t k = kn0 + lane + i * 32;
-              if (k < kn1)
-                cpa16(static_cast<uint32_t>(__cvta_generic_to_shared(slot + lane + i * 32)),
-                      srcn + k * 16);
+              int64_t k = k0 + lane + i * 32;
+              if (k < k1) v[i] = slot[lane + i * 32];
             }
           }
-          cpa_commit();  // (an empty group past the end keeps the count uniform)
-        };
-        if (!smem_ok) {
-          // speculation missed (or none was issued): drop it, fetch the
-          // lookahead with the real row map
-          cpa_wait_all();
-          for (int t = 1; t <= kSmemSpec; ++t) issue(t);
-        }
-        for (int it = 0;;) {
-          uint8_t* dst = dst_base + j * P.out_row_bytes;
-#pragma unroll
-          for (int i = 0; i < kUnroll; ++i) {
-            int64_t k = k0 + lane + i * 32;
-            if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
-          }
-          s += s_step;
-          ++it;
-          if (s >= s_end) break;
-          j = qdiv(s, spr);
-          k0 = (s - j * spr) * kSeg;
-          k1 = imin64(k0 + kSeg, wpr);
-          asm volatile("cp.async.wait_group %0;" ::"n"(kSmemSpec - 1) : "memory");
-          const uint4* slot = seg_smem(it - 1);
-#pragma unroll
-          for (int i = 0; i < kUnroll; ++i) {
-            int64_t k = k0 + lane + i * 32;
-            if (k < k1) v[i] = slot[lane + i * 32];
-          }
-          issue(it + kSmemSpec);  // into the slot read last iteration
-        }
-      } else {
-        for (;;) {
-          uint8_t* dst = dst_base + j * P.out_row_bytes;
-#pragma unroll
-          for (int i = 0; i < kUnroll; ++i) {
-            int64_t k = k0 + lane + i * 32;
-            if (k < k1) st_vec<VW>(dst + k * VW, v[i]);
-          }
-          s += s_step;
-          if (s >= s_end) break;
-          j = qdiv(s, spr);
-          k0 = (s - j * spr) * kSeg;
-          k1 = imin64(k0 + kSeg, wpr);
+        } else {
           const uint8_t* src = row_src(P, row_of(j));
 #pragma unroll
           for (int i = 0; i < kUnroll; ++i) {
@@ -1285,22 +1246,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   if (TF_ABL & 2) return;
   __syncthreads();
   if (sh.flagmode) {
-    // Fast path: each copy CTA orders its payload stores (cumulative over
-    // the CTA through the barrier above) before its increment of the slot's
-    // completion counter; the host takes the descriptor the controller
-    // posted once the counter has moved by the descriptor's CTA count. The
-    // controller committed the producer state meanwhile. No last-CTA
-    // election, no round trip and no host-memory access on the critical path.
+    // Fast path: each copy CTA orders its payload stores before its
+    // completion byte (the host takes the descriptor the controller posted
+    // once every byte is set). The controller committed the producer state
+    // meanwhile. No last-CTA election, no round trip on the critical path.
     if (tid == 0) {
       if (sh.publish && cb >= 0) {
 #if TF_FLAG_FENCE_SYS
         fence_acq_rel_sys();
 #else
-        // gpu scope: the staging copy engine reads the counter and, later,
-        // the payload through L2, so ordering at gpu scope is what it sees
+        // gpu scope, as the last-CTA publish: the payload is in L2 before
+        // the byte leaves, and the D2H copy engine reads through L2
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #endif
-        red_add_gpu(slot_done(P, sh.slot_idx), 1u);
+        st_relaxed_sys_u8(P.done_flags + sh.slot_idx * kMaxFlagCtas + cb, 1);
       }
       if (!kCtl && readers_before == uint32_t(cg) - 1) {
         // the last CTA to read the snapshot: every CTA of this launch holds
@@ -1795,20 +1754,18 @@ __global__ void publish_kernel(CapParams P, tf_descriptor d) {
     status = TF_ERR_META_RING_FULL;  // rings.py:327-330
   } else {
     uint64_t slot = c->meta_head % P.slots;
-    uint64_t* w = reinterpret_cast<uint64_t*>(P.meta + slot * kMetaStride);
-    // rings.py:334-335: the slot's previous descriptor must have been
-    // consumed (its sequence behind the consumer's meta_tail)
-    const uint64_t prev = w[3];
-    if (prev != TF_READY_SENTINEL && prev >= mtail) {
-      status = TF_ERR_PROTOCOL;
+    uint64_t* w = reinterpret_cast<uint64_t*>(P.meta + slot * TF_DESCRIPTOR_SIZE);
+    if (ld_relaxed_sys(w + 3) != TF_READY_SENTINEL) {
+      status = TF_ERR_PROTOCOL;  // rings.py:334-335
       c->errors |= TF_DEVERR_PROTOCOL;
     } else {
       seq = c->meta_head;
       d.ready_seq = seq;
-      d.flags &= (1u << TF_DESC_CTA_SHIFT) - 1u;  // no completion counter
       uint64_t* s = reinterpret_cast<uint64_t*>(&d);
       d.checksum = tf_desc_checksum(s);
-      for (int i = 0; i < 8; ++i) w[i] = s[i];
+      for (int i = 0; i < 8; ++i)
+        if (i != 3) st_relaxed_sys(w + i, s[i]);
+      st_relaxed_sys(w + 3, seq);
       c->meta_head = seq + 1;
     }
   }
@@ -1833,9 +1790,10 @@ static CapParams base_params(tf_ring* r) {
   P.payload = r->payload;
   P.cap = r->cfg.payload_capacity;
   P.slots = r->cfg.meta_slots;
-  P.meta = r->dmeta;
+  P.meta = r->meta;
   P.dcons = r->dcons;
   P.ctl = r->ctl;
+  P.done_flags = r->done_flags;
   P.timeout_ns = r->cfg.wait_timeout_ns ? r->cfg.wait_timeout_ns : 30000000000ull;
   return P;
 }
@@ -1883,9 +1841,8 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     if (r->payload) cudaFree(r->payload);
     if (r->ctl) cudaFree(r->ctl);
     if (r->dcons) cudaFree(r->dcons);
-    if (r->dmeta) cudaFree(r->dmeta);
-    if (r->hmirror) cudaFreeHost(r->hmirror);
-    if (r->poll_stream) cudaStreamDestroy((cudaStream_t)r->poll_stream);
+    if (r->meta) cudaFreeHost(r->meta);
+    if (r->done_flags) cudaFreeHost(r->done_flags);
     if (r->ctl_host) cudaFreeHost(r->ctl_host);
     if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
     delete r;
@@ -1898,25 +1855,18 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     cudaGetLastError();
     return fail(TF_ERR_ALLOCATION);  // rings.py:155-160 AllocationError
   }
-  const size_t meta_bytes = size_t(cfg->meta_slots) * kMetaStride;
-  if (cudaHostAlloc((void**)&r->hmirror, meta_bytes, cudaHostAllocPortable) != cudaSuccess ||
+  size_t meta_bytes = size_t(cfg->meta_slots) * TF_DESCRIPTOR_SIZE;
+  if (cudaHostAlloc((void**)&r->meta, meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->done_flags, size_t(cfg->meta_slots) * kMaxFlagCtas,
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
       cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
     tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_ALLOCATION);
   }
-  if (cudaMalloc(&r->dmeta, meta_bytes) != cudaSuccess) {
-    tf_set_error("device meta ring allocation failed");
-    cudaGetLastError();
-    return fail(TF_ERR_ALLOCATION);
-  }
-  memset(r->hmirror, 0, meta_bytes);
+  memset(r->meta, 0, meta_bytes);
+  memset(r->done_flags, 0, size_t(cfg->meta_slots) * kMaxFlagCtas);
   for (uint32_t s = 0; s < cfg->meta_slots; ++s)  // rings.py:213-215
-    reinterpret_cast<uint64_t*>(r->hmirror + size_t(s) * kMetaStride)[3] = TF_READY_SENTINEL;
-  if (cudaMemcpy(r->dmeta, r->hmirror, meta_bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
-    tf_set_error("device meta ring init failed");
-    return fail(TF_ERR_CUDA);
-  }
-  r->done_base.assign(cfg->meta_slots, 0u);
+    reinterpret_cast<uint64_t*>(r->meta + size_t(s) * TF_DESCRIPTOR_SIZE)[3] = TF_READY_SENTINEL;
   if (cudaMalloc(&r->ctl, sizeof(DevCtl)) != cudaSuccess ||
       cudaMalloc(&r->dcons, sizeof(DevConsumer)) != cudaSuccess) {
     tf_set_error("device control block allocation failed");
@@ -1946,11 +1896,6 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     return fail(TF_ERR_CUDA);
   }
   r->snap_stream = s;
-  if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) {
-    tf_set_error("poll stream create failed");
-    return fail(TF_ERR_CUDA);
-  }
-  r->poll_stream = s;
   if (kSmemSpec > 0 && kSpecSmemBytes > 48 * 1024 &&
       cudaFuncSetAttribute(capture_kernel<MODE_COPY, 16, 0, 0>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1972,9 +1917,8 @@ extern "C" int tf_ring_destroy(tf_ring* r) {
   cudaFree(r->payload);
   cudaFree(r->ctl);
   cudaFree(r->dcons);
-  if (r->poll_stream) cudaStreamDestroy((cudaStream_t)r->poll_stream);
-  cudaFree(r->dmeta);
-  cudaFreeHost(r->hmirror);
+  cudaFreeHost(r->meta);
+  cudaFreeHost(r->done_flags);
   cudaFreeHost(r->ctl_host);
   delete r;
   return TF_OK;
@@ -1985,16 +1929,9 @@ extern "C" int tf_ring_payload_ptr(tf_ring* r, void** p) {
   *p = r->payload;
   return TF_OK;
 }
-static int refresh_mirror(tf_ring* r, uint64_t count);
-
-// The host mirror of the meta ring (kMetaStride per slot), refreshed first
-// over the slots the consumer has not taken yet.
 extern "C" int tf_ring_meta_ptr(tf_ring* r, void** p) {
   if (!r || !p) return TF_ERR_VALUE;
-  std::lock_guard<std::mutex> g(r->mu);
-  int rc = refresh_mirror(r, r->cfg.meta_slots);
-  if (rc) return rc;
-  *p = r->hmirror;
+  *p = r->meta;
   return TF_OK;
 }
 
@@ -2350,6 +2287,11 @@ extern "C" int tf_ring_publish(tf_ring* r, void* stream, const tf_descriptor* d,
 // ---------------------------------------------------------------------------
 // host: consumer role
 // ---------------------------------------------------------------------------
+static inline uint64_t slot_ready(const tf_ring* r, uint64_t slot) {
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE) + 3;
+  return __atomic_load_n(p, __ATOMIC_ACQUIRE);
+}
+
 // Stream-ordered u64 write into device memory: cuStreamWriteValue64 via
 // the driver entry point (the value rides in the command, no host buffer);
 // a pinned-slot cudaMemcpyAsync if stream memory ops are unavailable.
@@ -2414,93 +2356,51 @@ static bool slot_verified(const uint8_t* raw, tf_descriptor* d) {
   return true;
 }
 
-// Copy the next `count` slots from meta_tail (the ones the consumer has not
-// taken) from the device meta ring into the host mirror: one or two small
-// D2H copies on the ring's high-priority poll stream. Caller holds r->mu.
-static int refresh_mirror(tf_ring* r, uint64_t count) {
-  const uint64_t slots = r->cfg.meta_slots;
-  count = std::min(count, slots);
-  if (!count) return TF_OK;
-  int rc = set_device(r->device);
-  if (rc) return rc;
-  RelaxedCaptureMode relaxed;  // may run while another thread records a graph
-  const auto t0 = std::chrono::steady_clock::now();
-  const uint64_t first = r->meta_tail % slots;
-  const uint64_t n1 = std::min(count, slots - first);
-  cudaStream_t s = (cudaStream_t)r->poll_stream;
-  CUDA_TRY(cudaMemcpyAsync(r->hmirror + first * kMetaStride, r->dmeta + first * kMetaStride,
-                           n1 * kMetaStride, cudaMemcpyDeviceToHost, s));
-  if (count > n1)
-    CUDA_TRY(cudaMemcpyAsync(r->hmirror, r->dmeta, (count - n1) * kMetaStride,
-                             cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  const uint64_t ns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
-      std::chrono::steady_clock::now() - t0).count());
-  r->refreshes.fetch_add(1, std::memory_order_relaxed);
-  r->refresh_ns.fetch_add(ns, std::memory_order_relaxed);
-  if (ns > r->refresh_max_ns.load(std::memory_order_relaxed))
-    r->refresh_max_ns.store(ns, std::memory_order_relaxed);  // caller holds r->mu
-  return TF_OK;
-}
-
-// Slots refreshed per poll: enough for one drain batch; more arrive with
-// the next refresh.
-constexpr uint64_t kRefreshSlots = 256;
-
-// Slot `slot` holds descriptor number `seq` (ready_seq == seq, checksum
-// verified) and, for a capture posted before its copy finished, every one
-// of its CTAs has bumped the slot's completion counter past the counts of
-// the slot's earlier captures. The CTA count is stripped from the flags.
-static bool slot_complete(const tf_ring* r, uint64_t slot, uint64_t seq, tf_descriptor* d) {
-  const uint8_t* line = r->hmirror + slot * kMetaStride;
-  if (!slot_verified(line, d) || d->ready_seq != seq) return false;
+// A posted slot is complete when its checksum verifies and, for a capture
+// posted before its copy finished, every CTA has set its completion byte.
+// The CTA count is stripped from the flags handed out.
+static bool slot_complete(const tf_ring* r, uint64_t slot, tf_descriptor* d) {
+  if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, d)) return false;
   const uint32_t n = d->flags >> TF_DESC_CTA_SHIFT;
-  if (n) {
-    uint32_t done;
-    memcpy(&done, line + kMetaDoneOff, 4);
-    if (done - r->done_base[slot] != n) return false;
+  if (n) {  // 8 completion bytes per load
+    const uint8_t* f = r->done_flags + slot * kMaxFlagCtas;
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(f);
+    uint32_t i = 0;
+    for (; i + 8 <= n; i += 8)
+      if (__atomic_load_n(w + i / 8, __ATOMIC_ACQUIRE) != 0x0101010101010101ull) return false;
+    for (; i < n; ++i)
+      if (__atomic_load_n(f + i, __ATOMIC_ACQUIRE) != 1) return false;
   }
   d->flags &= (1u << TF_DESC_CTA_SHIFT) - 1u;
   return true;
 }
 
 int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
-                     uint32_t* n, bool consume, bool refresh) {
-  if (refresh) {
-    int rc = refresh_mirror(r, std::min<uint64_t>(max_entries, kRefreshSlots));
-    if (rc) return rc;
-  }
+                     uint32_t* n, bool consume) {
   uint32_t got = 0;
   const uint64_t slots = r->cfg.meta_slots;
   uint64_t tail = r->meta_tail;
   bool advanced = false;
   while (got < max_entries && got < slots) {
-    const uint64_t slot = tail % slots;
+    uint64_t slot = tail % slots;
+    uint64_t ready = slot_ready(r, slot);
+    if (ready == TF_READY_SENTINEL) break;
     tf_descriptor d;
-    // the consumer's next sequence number: a slot still holding an older
-    // descriptor, or one whose CTAs are still copying, is not ready
-    const uint64_t want = r->consumed + (consume ? 0 : got);
-    if (!slot_complete(r, slot, want, &d)) {
-      // a verified descriptor out of sequence is a protocol violation
-      // (rings.py:397-401); an older one is just not ready yet
-      tf_descriptor o;
-      const uint8_t* line = r->hmirror + slot * kMetaStride;
-      if (consume && slot_verified(line, &o) && o.ready_seq > want &&
-          o.ready_seq != TF_READY_SENTINEL) {
+    // words may still be landing: accept only a slot whose checksum
+    // verifies (and whose capture CTAs have all reported)
+    if (!slot_complete(r, slot, &d)) break;
+    if (consume) {
+      if (d.ready_seq != r->consumed) {  // rings.py:397-401
         tf_set_error("descriptor sequence %llu out of order, expected %llu",
-                     (unsigned long long)o.ready_seq, (unsigned long long)want);
+                     (unsigned long long)d.ready_seq, (unsigned long long)r->consumed);
         *n = got;
         return TF_ERR_PROTOCOL;
       }
-      break;
-    }
-    if (consume) {
       const uint32_t n_ctas = reinterpret_cast<const tf_descriptor*>(
-          r->hmirror + slot * kMetaStride)->flags >> TF_DESC_CTA_SHIFT;
-      r->done_base[slot] += n_ctas;
-      // the mirror slot reads as free again (rings.py:402-404)
-      uint64_t* rp = reinterpret_cast<uint64_t*>(r->hmirror + slot * kMetaStride) + 3;
-      *rp = TF_READY_SENTINEL;
+          r->meta + slot * TF_DESCRIPTOR_SIZE)->flags >> TF_DESC_CTA_SHIFT;
+      if (n_ctas) memset(r->done_flags + slot * kMaxFlagCtas, 0, n_ctas);
+      uint64_t* rp = reinterpret_cast<uint64_t*>(r->meta + slot * TF_DESCRIPTOR_SIZE) + 3;
+      __atomic_store_n(rp, TF_READY_SENTINEL, __ATOMIC_RELEASE);
       r->meta_tail = ++tail;
       r->consumed += 1;
       advanced = true;
@@ -2534,7 +2434,7 @@ extern "C" int tf_ring_ready_entries(tf_ring* r, uint64_t* n) {
   if (!r || !n) return TF_ERR_VALUE;
   std::lock_guard<std::mutex> g(r->mu);
   uint32_t k = 0;
-  int rc = tf_internal_poll(r, r->cfg.meta_slots, nullptr, &k, false, true);
+  int rc = tf_internal_poll(r, r->cfg.meta_slots, nullptr, &k, false);
   *n = k;
   return rc;
 }
@@ -2542,12 +2442,15 @@ extern "C" int tf_ring_ready_entries(tf_ring* r, uint64_t* n) {
 extern "C" int tf_ring_ready_bytes(tf_ring* r, uint64_t* n) {
   if (!r || !n) return TF_ERR_VALUE;
   std::lock_guard<std::mutex> g(r->mu);
-  std::vector<tf_descriptor> ds(r->cfg.meta_slots);
-  uint32_t k = 0;
-  int rc = tf_internal_poll(r, r->cfg.meta_slots, ds.data(), &k, false, true);
-  if (rc) return rc;
   uint64_t total = 0;
-  for (uint32_t i = 0; i < k; ++i) total += ds[i].payload_len;
+  const uint64_t slots = r->cfg.meta_slots;
+  for (uint64_t i = 0; i < slots; ++i) {
+    uint64_t slot = (r->meta_tail + i) % slots;
+    tf_descriptor d;
+    if (slot_ready(r, slot) == TF_READY_SENTINEL || !slot_complete(r, slot, &d))
+      break;
+    total += d.payload_len;
+  }
   *n = total;
   return TF_OK;
 }
@@ -2555,13 +2458,13 @@ extern "C" int tf_ring_ready_bytes(tf_ring* r, uint64_t* n) {
 extern "C" int tf_ring_peek_ready(tf_ring* r, uint32_t max_entries, tf_descriptor* out, uint32_t* n) {
   if (!r || !n) return TF_ERR_VALUE;
   std::lock_guard<std::mutex> g(r->mu);
-  return tf_internal_poll(r, max_entries, out, n, false, true);
+  return tf_internal_poll(r, max_entries, out, n, false);
 }
 
 extern "C" int tf_ring_poll_ready(tf_ring* r, uint32_t max_entries, tf_descriptor* out, uint32_t* n) {
   if (!r || !n) return TF_ERR_VALUE;
   std::lock_guard<std::mutex> g(r->mu);
-  return tf_internal_poll(r, max_entries, out, n, true, true);
+  return tf_internal_poll(r, max_entries, out, n, true);
 }
 
 int tf_internal_release(tf_ring* r, uint64_t offset, uint64_t length, bool push) {

@@ -21,9 +21,7 @@
 #pragma once
 #include <stdint.h>
 
-#include <atomic>
 #include <deque>
-#include <vector>
 #include <map>
 #include <mutex>
 
@@ -31,11 +29,11 @@
 
 #include "ring2_core.h"
 
-// Host threads of the consumer side (poll refreshes, staging threads) make
-// stream-synchronising calls on their own private streams. Under another
-// thread's global-mode CUDA graph capture (torch.cuda.graph's default) those
-// calls would invalidate the capture, so these threads run in relaxed
-// capture mode: nothing they touch is being captured.
+// Host threads of the consumer side (staging threads) make stream-
+// synchronising calls on their own private streams. Under another thread's
+// global-mode CUDA graph capture (torch.cuda.graph's default) those calls
+// would invalidate the capture, so these threads run in relaxed capture
+// mode: nothing they touch is being captured.
 struct RelaxedCaptureMode {
   cudaStreamCaptureMode prev = cudaStreamCaptureModeRelaxed;
   RelaxedCaptureMode() { cudaThreadExchangeStreamCaptureMode(&prev); }
@@ -66,14 +64,7 @@ struct alignas(128) ProdSnap {
   uint64_t used, head, tail, pad1[5];
 };
 constexpr int kSnapReplicas = 8;
-// Device meta ring: one kMetaStride line per slot, the 64-B descriptor then
-// a u32 completion counter that every copy CTA of a flag-mode capture bumps
-// after its payload stores. The ring lives in HBM: a capture kernel never
-// writes host memory (under a saturated D2H link such writes hold the
-// kernel's completion for several microseconds; scripts/exp_fixed.cu).
-constexpr int kMetaStride = 128;
-constexpr int kMetaDoneOff = 64;
-constexpr int kMaxFlagCtas = 65535;  // copy CTAs a descriptor's flags can count
+constexpr int kMaxFlagCtas = 512;   // completion bytes per meta slot
 
 struct alignas(128) DevCtl {
   // allocator (producer role)
@@ -116,16 +107,11 @@ struct tf_ring {
   int device = 0;
   tf_ring_config cfg{};
   uint8_t* payload = nullptr;     // device
-  // meta ring in device memory (kMetaStride per slot: descriptor + done
-  // counter) and its pinned host mirror, refreshed by small D2H copies on
-  // poll_stream when the consumer looks for work
-  uint8_t* dmeta = nullptr;
-  uint8_t* hmirror = nullptr;
-  void* poll_stream = nullptr;
-  std::vector<uint32_t> done_base;  // per slot: CTA completions of earlier captures
-  // mirror refreshes: count, summed and worst wall time (diagnostics; the
-  // small D2H can queue behind staging transfers on the copy engine)
-  std::atomic<uint64_t> refreshes{0}, refresh_ns{0}, refresh_max_ns{0};
+  uint8_t* meta = nullptr;        // host pinned mapped (device alias == same VA)
+  // per meta slot, one completion byte per capture CTA (host pinned mapped):
+  // fast-path captures post their descriptor early and every CTA sets its
+  // byte after its payload stores; the host takes the slot once all are set
+  uint8_t* done_flags = nullptr;
   DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
   DevCtl* ctl_host = nullptr;     // pinned, host-mapped snapshot target
@@ -141,10 +127,8 @@ struct tf_ring {
 };
 
 // cross-TU helpers (ring2.cu)
-// caller holds r->mu; refresh=true first copies the pending window of the
-// device meta ring into the host mirror
 int tf_internal_poll(tf_ring* r, uint32_t max_entries, tf_descriptor* out,
-                     uint32_t* n, bool consume, bool refresh);
+                     uint32_t* n, bool consume);
 // release without pushing L to the device (the staging stream already
 // wrote it behind the D2H)
 int tf_internal_release(tf_ring* r, uint64_t offset, uint64_t length, bool push);

@@ -277,6 +277,8 @@ struct tf_stager {
   std::vector<uint8_t*> paged_pool;
   uint32_t outstanding_paged = 0;
   uint64_t outstanding_handoff = 0;  // pinned buffers held by the consumer
+  uint64_t max_split_bufs = 0;       // most chunk buffers one split capture took
+  uint64_t pageable_budget = 0;      // paged-out bytes the stage thread may run ahead by
   std::atomic<int> bg_error{0};
   std::atomic<uint32_t> completion_phase{0}, stage_phase{0};  // diagnostics
   std::string bg_errmsg;
@@ -318,6 +320,8 @@ extern "C" int tf_stager_create(tf_ring* ring, const tf_drain_config* cfg, tf_st
   st->ring = ring;
   st->cfg = *cfg;
   if (!st->cfg.stage_queue_slots) st->cfg.stage_queue_slots = 16;  // exporter.py:32
+  st->pageable_budget = uint64_t(32) << 30;
+  if (const char* e = getenv("TF_PAGEABLE_BUDGET_MIB")) st->pageable_budget = strtoull(e, nullptr, 10) << 20;
   st->device = ring->device;
   if (cudaSetDevice(st->device) != cudaSuccess) {
     delete st;
@@ -394,20 +398,9 @@ static uint32_t reason_for(tf_stager* st, uint64_t entries, uint64_t bytes,
   return TF_REASON_NONE;
 }
 
-// The ring's ready descriptors as the host mirror shows them; refresh=true
-// first copies the pending window of the device meta ring (one small D2H on
-// the ring's poll stream). A drain iteration refreshes once and then peeks
-// and polls that same snapshot.
-static int ring_ready(tf_ring* r, uint32_t max, tf_descriptor* out, uint32_t* n, bool consume,
-                      bool refresh) {
-  std::lock_guard<std::mutex> g(r->mu);
-  return tf_internal_poll(r, max, out, n, consume, refresh);
-}
-
 static void ready_summary(tf_stager* st, std::vector<tf_descriptor>& tmp, uint32_t* n, uint64_t* bytes) {
   tmp.resize(st->ring->cfg.meta_slots);
-  *n = 0;
-  if (ring_ready(st->ring, (uint32_t)tmp.size(), tmp.data(), n, false, true)) *n = 0;
+  tf_ring_peek_ready(st->ring, (uint32_t)tmp.size(), tmp.data(), n);
   uint64_t b = 0;
   for (uint32_t i = 0; i < *n; ++i) b += tmp[i].payload_len;
   *bytes = b;
@@ -449,7 +442,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
   *out = nullptr;
   std::vector<tf_descriptor> ready(st->ring->cfg.meta_slots);
   uint32_t n = 0;
-  int rc = ring_ready(st->ring, (uint32_t)ready.size(), ready.data(), &n, false, false);
+  int rc = tf_ring_peek_ready(st->ring, (uint32_t)ready.size(), ready.data(), &n);
   if (rc) return rc;
   if (n == 0) return TF_OK;
   if (st->free_bufs.empty()) {
@@ -476,6 +469,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
                    (unsigned long long)k, st->free_bufs.size());
       return TF_ERR_STAGING_EXHAUSTED;
     }
+    st->max_split_bufs = std::max<uint64_t>(st->max_split_bufs, k);
     for (uint64_t c = 0; c < k; ++c) {
       chunk_bufs.push_back(st->free_bufs.back());
       st->free_bufs.pop_back();
@@ -504,7 +498,7 @@ static int issue_batch(tf_stager* st, uint32_t reason, Batch** out) {
 
   std::vector<tf_descriptor> got(take);
   uint32_t polled = 0;
-  rc = ring_ready(st->ring, take, got.data(), &polled, true, false);
+  rc = tf_ring_poll_ready(st->ring, take, got.data(), &polled);
   if (rc || polled != take) {
     if (chunk_bufs.empty()) st->free_bufs.push_back(b);
     for (uint32_t c : chunk_bufs) st->free_bufs.push_back(c);
@@ -799,9 +793,6 @@ extern "C" int tf_stager_stats_get(tf_stager* st, tf_stager_stats* out) {
   out->outstanding_paged = st->outstanding_paged;
   out->completion_phase = st->completion_phase.load();
   out->stage_phase = st->stage_phase.load();
-  out->meta_refreshes = st->ring->refreshes.load(std::memory_order_relaxed);
-  out->meta_refresh_ns = st->ring->refresh_ns.load(std::memory_order_relaxed);
-  out->meta_refresh_max_ns = st->ring->refresh_max_ns.load(std::memory_order_relaxed);
   return TF_OK;
 }
 
@@ -912,14 +903,12 @@ static void drain_loop(tf_stager* st) {
         }
       }
     }
-    // every iteration refreshes the mirror with a small D2H (driver calls):
-    // back off while nothing new arrives (10 -> 160 us), poll at once after
-    // progress or under a flush
-    if (did || st->flush_req.load()) {
+    if (did) {
       idle = 0;
+    } else if (++idle < 2000) {
+      cpu_relax();
     } else {
-      idle = std::min(idle + 1, 5);
-      std::this_thread::sleep_for(std::chrono::microseconds(5 << idle));
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   }
   st->drain_done = true;
@@ -994,8 +983,11 @@ static void stage_loop(tf_stager* st) {
       // holds must never starve the drain. So a batch is handed off only
       // while at least half the pool stays with the engine; otherwise it is
       // copied out, and its buffer returns at once.
+      // (and never into the buffers the largest split capture seen so far
+      // needs at once: a split capture waits for all of its chunks' buffers)
       handoff_ok = st->cfg.page_out == TF_PAGE_OUT_HANDOFF &&
-                   2 * (st->outstanding_handoff + 1) <= st->bufs.size();
+                   2 * (st->outstanding_handoff + 1) <= st->bufs.size() &&
+                   st->outstanding_handoff + 1 + st->max_split_bufs <= st->bufs.size();
       if ((st->cfg.page_out == TF_PAGE_OUT_COPY || !handoff_ok) && b->chunk_bufs.empty())
         dst = paged_alloc(st);
       if (handoff_ok && b->chunk_bufs.empty()) st->outstanding_handoff += 1;
@@ -1045,7 +1037,15 @@ static void stage_loop(tf_stager* st) {
       note_transient(st);
       st->cv.notify_all();
       st->stage_phase = 3;
-      st->cv.wait(g, [&] { return st->out_q.size() < st->cfg.stage_queue_slots || st->stop_req; });
+      // The queue bound (exporter.py:32) applies while the paged-out bytes
+      // stay under the budget; past it the stage thread runs ahead of the
+      // consumer into pageable memory. A Python consumer can be starved of
+      // the GIL by an inference thread blocked in a CUDA call while the
+      // device waits for ring space; the ring must still drain then.
+      st->cv.wait(g, [&] {
+        return st->out_q.size() < st->cfg.stage_queue_slots ||
+               st->pageable_in_flight <= st->pageable_budget || st->stop_req;
+      });
       st->stage_phase = 0;
       st->out_q.push_back(pb);
       st->cv.notify_all();
