@@ -52,8 +52,13 @@ def parse():
     p.add_argument("--seq", type=int, default=512)
     p.add_argument("--staging", default="copy-engine",
                    choices=["copy-engine", "mapped"])
-    p.add_argument("--legs", default="value,e2e,model,c2,gpt2,cpu")
+    p.add_argument("--legs", default="value,e2e,model,gpt2,cpu",
+                   help="also: c2 (SURVEY C2 64x512 prefill + decode, HF eager), "
+                        "overload, e2efile")
     p.add_argument("--e2e-steps", type=int, default=8)
+    p.add_argument("--sink-dir", default="gpurun_out/e2e_sink",
+                   help="dataset directory of the e2efile leg (deleted afterwards)")
+    p.add_argument("--sink-threads", type=int, default=8)
     p.add_argument("--page-out", default="handoff",
                    choices=["copy", "handoff"],
                    help="exporter page-out for the e2e and model legs")
@@ -76,6 +81,23 @@ def parse():
 # distributed plumbing (replicas: barrier + max-over-ranks timing only)
 # ---------------------------------------------------------------------------
 _T0 = time.perf_counter()
+
+
+def guarded(name, fn, *a):
+    """Run an auxiliary leg; a failure is recorded in the JSON line instead
+    of losing the headline (value / e2e / roofline) with it."""
+    try:
+        return fn(*a)
+    except Exception as exc:  # noqa: BLE001 -- reported, not hidden
+        import traceback
+        log(f"leg {name} failed:\n{traceback.format_exc()}")
+        try:
+            import torch
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+        except Exception:
+            pass
+        return {"error": f"{type(exc).__name__}: {exc}"[:500]}
 
 
 def log(msg: str) -> None:
@@ -468,7 +490,12 @@ def leg_value(args, dist, dev):
 # ---------------------------------------------------------------------------
 # leg: e2e through the public API with host inputs
 # ---------------------------------------------------------------------------
-def leg_e2e(args, dist, dev):
+def leg_e2e(args, dist, dev, sink_dir=None):
+    """``sink_dir``: write the dataset format through NativeFileSink
+    (O_DIRECT sidecar where the filesystem allows it) instead of NullSink;
+    the sink's write time is then inside the timed region."""
+    import shutil
+
     import torch
 
     from paper_2605_11093_b200 import (DrainConfig, NullSink, PolicyConfig,
@@ -479,7 +506,12 @@ def leg_e2e(args, dist, dev):
     cfg = llama3_8b_config()
     reg = llama_registry(cfg, ("mlp_act", "resid_post"))
     step_bytes = B * T * (HIDDEN + FFN) * 2 * LAYERS
-    sink = NullSink()
+    if sink_dir:
+        from paper_2605_11093_b200.sinks import NativeFileSink
+        shutil.rmtree(sink_dir, ignore_errors=True)
+        sink = NativeFileSink(sink_dir, threads=args.sink_threads, direct=True)
+    else:
+        sink = NullSink()
     obs = Observer(reg, ring=RingConfig(2 * step_bytes, 1024),
                    drain=DrainConfig(min_ready_entries=1, min_ready_bytes=1,
                                      max_wait=1e-4,
@@ -532,9 +564,15 @@ def leg_e2e(args, dist, dev):
     got = sink.bytes_written - bytes0
     obs.check_device()
     obs.close()
-    return {"bytes": got, "elapsed_s": wall, "device_span_s": e0.elapsed_time(e1) * 1e-3,
-            "steps": n, "h2d_per_step": step_bytes, "d2h_per_step": step_bytes,
-            "records": sink.records_written}
+    out = {"bytes": got, "elapsed_s": wall, "device_span_s": e0.elapsed_time(e1) * 1e-3,
+           "steps": n, "h2d_per_step": step_bytes, "d2h_per_step": step_bytes,
+           "records": sink.records_written}
+    if sink_dir:
+        out["sink"] = {"kind": "NativeFileSink", "dir": sink_dir, "o_direct": sink.direct,
+                       "threads": args.sink_threads}
+        sink.close()
+        shutil.rmtree(sink_dir, ignore_errors=True)
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -1297,25 +1335,36 @@ def main():
                "h2d_bytes_per_step": e["h2d_per_step"],
                "d2h_bytes_per_step": e["d2h_per_step"],
                "steps": e["steps"], "records": e["records"]}
+    e2e_file = None
+    if "e2efile" in legs:
+        log("leg e2e (NativeFileSink)")
+        e = leg_e2e(args, dist, dev, sink_dir=f"{args.sink_dir}_r{dist.rank}")
+        eb = dist.reduce([e["bytes"]], "sum")[0]
+        et = dist.reduce([e["elapsed_s"]], "max")[0]
+        e2e_file = {"value": eb / et / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": e["h2d_per_step"],
+                    "d2h_bytes_per_step": e["d2h_per_step"],
+                    "steps": e["steps"], "records": e["records"], "sink": e["sink"]}
+        log(f"e2e file sink: {json.dumps(e2e_file)}")
     log("build model")
     llama = build_model(dev) if ("model" in legs or "c2" in legs) else None
     log("leg model")
-    model = leg_model(args, dist, dev, llama) if "model" in legs else None
+    model = guarded("model", leg_model, args, dist, dev, llama) if "model" in legs else None
     log(f"model: {json.dumps(model)}")
     log("leg c2")
-    c2 = leg_c2(args, dist, dev, llama) if "c2" in legs else None
+    c2 = guarded("c2", leg_c2, args, dist, dev, llama) if "c2" in legs else None
     log(f"c2: {json.dumps(c2)}")
     del llama
     torch.cuda.empty_cache()
     overload = None
     if "overload" in legs:
         log("leg overload")
-        overload = leg_overload(args, dist, dev)
+        overload = guarded("overload", leg_overload, args, dist, dev)
         log(f"overload: {json.dumps(overload)}")
     log("leg gpt2")
-    gpt2 = leg_gpt2(args, dist, dev) if "gpt2" in legs else None
+    gpt2 = guarded("gpt2", leg_gpt2, args, dist, dev) if "gpt2" in legs else None
     log(f"gpt2: {json.dumps(gpt2)}")
-    if model:
+    if model and "error" not in model:
         for mode in model:
             for key in ("resid", "resid_mlp"):
                 model[mode][key]["overhead_pct_max_over_ranks"] = dist.reduce(
@@ -1385,6 +1434,7 @@ def main():
             "overload": overload,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_file_sink": e2e_file,
             "pcie_bidirectional": bidir,
             "gpu_launches": v["launches"] * dist.world,
             "clocks": v["clocks"],

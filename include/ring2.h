@@ -233,6 +233,12 @@ int tf_ring_release_payload(tf_ring* ring, uint64_t offset, uint64_t length);
 /* Wait until the device sees every release/poll made so far (the cursors
  * reach device memory through stream-ordered writes). */
 int tf_ring_sync_consumer(tf_ring* ring);
+/* Consumer-side totals the host already holds (no device access, no
+ * synchronisation): reserved bytes released (dead skips excluded) and
+ * descriptors consumed.
+ * Monotonic; the admission gate of eager captures polls it (no reference
+ * analogue: the reference producer raises instead of waiting). */
+int tf_ring_host_released(tf_ring* ring, uint64_t* bytes_released, uint64_t* consumed);
 
 /* ---- shared: rings.py:241-276 ------------------------------------------ */
 /* Snapshot; the caller must have synchronised the producer stream. */

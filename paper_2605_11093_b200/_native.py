@@ -191,6 +191,7 @@ _SIGS = [
     ("tf_ring_sync_consumer", C.c_int, [C.c_void_p]),
     ("tf_ring_get_state", C.c_int, [C.c_void_p, C.POINTER(CRingState)]),
     ("tf_ring_free_meta_slots", C.c_int, [C.c_void_p, u64p]),
+    ("tf_ring_host_released", C.c_int, [C.c_void_p, u64p, u64p]),
     ("tf_ring_would_fit", C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_int64, C.POINTER(C.c_int)]),
     ("tf_stager_create", C.c_int, [C.c_void_p, C.POINTER(CDrainConfig), C.POINTER(C.c_void_p)]),
     ("tf_stager_destroy", C.c_int, [C.c_void_p]),

@@ -251,6 +251,23 @@ __device__ __forceinline__ void load8(const uint8_t* p, float* f) {
     }
   }
 }
+// the same, from 16-B words already in registers (f32: two words)
+template <int DT>
+__device__ __forceinline__ void cvt8(const uint4* r, float* f) {
+  if constexpr (DT == TF_F32) {
+    f[0] = __uint_as_float(r[0].x); f[1] = __uint_as_float(r[0].y);
+    f[2] = __uint_as_float(r[0].z); f[3] = __uint_as_float(r[0].w);
+    f[4] = __uint_as_float(r[1].x); f[5] = __uint_as_float(r[1].y);
+    f[6] = __uint_as_float(r[1].z); f[7] = __uint_as_float(r[1].w);
+  } else {
+    const uint32_t w[4] = {r[0].x, r[0].y, r[0].z, r[0].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = bits_to_f(DT, w[i] & 0xFFFFu);
+      f[2 * i + 1] = bits_to_f(DT, w[i] >> 16);
+    }
+  }
+}
 template <int DT>
 __device__ __forceinline__ void store8(uint8_t* p, const float* f) {
   if constexpr (DT == TF_F32) {
@@ -1167,12 +1184,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           const uint8_t* src = row_src(P, row_of(j));
           uint8_t* dst = dst_base + j * P.out_row_bytes;
           if constexpr (VW == 8) {
-#pragma unroll 2
+            // the segment's loads all in flight before any conversion (as
+            // the copy path: ~64 KiB of reads outstanding per SM)
+            constexpr int NR = IN_DT == TF_F32 ? 2 : 1;  // 16-B words per 8 elements
+            uint4 raw[kUnroll][NR];
+#pragma unroll
+            for (int i = 0; i < kUnroll; ++i) {
+              int64_t k = k0 + lane + i * 32;
+              if (k < k1) {
+#pragma unroll
+                for (int q = 0; q < NR; ++q) raw[i][q] = ld_stream<16>(src + k * 8 * WI + 16 * q);
+              }
+            }
+#pragma unroll
             for (int i = 0; i < kUnroll; ++i) {
               int64_t k = k0 + lane + i * 32;
               if (k < k1) {
                 float f[8];
-                load8<IN_DT>(src + k * 8 * WI, f);
+                cvt8<IN_DT>(raw[i], f);
                 store8<OUT_DT>(dst + k * 8 * WO, f);
               }
             }
@@ -1193,16 +1222,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
           if (VW == 8) {
             const int64_t G8 = H / 8;
-            for (int64_t g = lane; g < G8; g += 32) {
-              float f[8];
-              load8<IN_DT>(src + g * 8 * WI, f);
+            constexpr int NR = IN_DT == TF_F32 ? 2 : 1;
+            constexpr int RU = IN_DT == TF_F32 ? kUnroll / 2 : kUnroll;  // loads in flight
+            for (int64_t g0 = lane; g0 < G8; g0 += 32 * RU) {
+              uint4 raw[RU][NR];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                sum += (double)f[e];
-                sq += (double)f[e] * (double)f[e];
-                mn = fminf(mn, f[e]);
-                mx = fmaxf(mx, f[e]);
-                amax = fmaxf(amax, fabsf(f[e]));
+              for (int u = 0; u < RU; ++u) {
+                const int64_t g = g0 + int64_t(u) * 32;
+                if (g < G8) {
+#pragma unroll
+                  for (int q = 0; q < NR; ++q) raw[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < RU; ++u) {
+                if (g0 + int64_t(u) * 32 < G8) {
+                  float f[8];
+                  cvt8<IN_DT>(raw[u], f);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    sum += (double)f[e];
+                    sq += (double)f[e] * (double)f[e];
+                    mn = fminf(mn, f[e]);
+                    mx = fmaxf(mx, f[e]);
+                    amax = fmaxf(amax, fabsf(f[e]));
+                  }
+                }
               }
             }
           } else {
@@ -2504,6 +2549,14 @@ uint64_t tf_internal_l_after_all(tf_ring* r) {
 extern "C" int tf_ring_release_payload(tf_ring* r, uint64_t offset, uint64_t length) {
   if (!r) return TF_ERR_VALUE;
   return tf_internal_release(r, offset, length, true);
+}
+
+extern "C" int tf_ring_host_released(tf_ring* r, uint64_t* bytes_released, uint64_t* consumed) {
+  if (!r) return TF_ERR_VALUE;
+  std::lock_guard<std::mutex> g(r->mu);
+  if (bytes_released) *bytes_released = r->bytes_released;  // reservations, no dead skips
+  if (consumed) *consumed = r->consumed;
+  return TF_OK;
 }
 
 extern "C" int tf_ring_sync_consumer(tf_ring* r) {

@@ -145,6 +145,18 @@ class Observer:
         self.active = persistent
         self.launches = 0
         self.steps = 0
+        # Admission gate of eager captures under completeness (see _admit):
+        # reserved bytes launched so far, released bytes last seen, the
+        # largest reservation (dead-skip slack), this step's expected
+        # reservation per hook, and whether a CUDA graph is being recorded
+        self.wait_timeout = wait_timeout
+        self._launched = 0
+        self._released = 0
+        self._max_need = 0
+        self._need: dict[str, list[int]] = {}
+        self._recording = False
+        self.gate_waits = 0
+        self.gate_wait_s = 0.0
 
     # -- session -----------------------------------------------------------
 
@@ -227,6 +239,16 @@ class Observer:
                      if m.hook_name in groups else m
                      for m in metas]
         self.fifo.extend(metas)
+        self._need = {}
+        if self.policy.mode == COMPLETENESS and not self.persistent and metas:
+            lens = metas.payload_lens() if isinstance(metas, StepMetas) else \
+                [m.expected_payload_len for m in metas]
+            names = [e[0] for e in metas.entries] if isinstance(metas, StepMetas) else \
+                [m.hook_name for m in metas]
+            for name, n in zip(names, lens):
+                self._need.setdefault(name, []).append((n + 15) & ~15)
+            for q in self._need.values():
+                q.reverse()  # popped from the end, in firing order
         s = stream if stream is not None else t.cuda.current_stream(self.device)
         with t.cuda.stream(s):
             busy = self._pinned.get("_busy")
@@ -374,9 +396,11 @@ class Observer:
                 obs.registry.commit_filter()
                 obs._was_active = obs.active
                 obs.active = True
+                obs._recording = True
 
             def __exit__(self_inner, *exc):
                 obs.active = obs._was_active
+                obs._recording = False
         return _Rec()
 
     def check_device(self) -> None:
@@ -430,6 +454,10 @@ class Observer:
             src, hook_id=hook_id, hook=hook, keep_ptr=keep.data_ptr(),
             keep_per_outer=per_outer, step_seq_ptr=self.step_buf.data_ptr(),
             full=self.policy.full_mode)
+        if self._need and not self._recording:
+            q = self._need.get(hook.name)
+            if q:
+                self._admit(q.pop())
         launch_capture(self.ring, args, stream)
         self.launches += 1
         dbg = self.debug_clone.get(hook_id)
@@ -438,6 +466,67 @@ class Observer:
             if flat_x.numel() > dbg.numel():
                 raise ConfigError("debug clone buffer too small")
             dbg[:flat_x.numel()].copy_(flat_x)
+
+
+    def _admit(self, need: int) -> None:
+        """Admission gate for eager captures under completeness.
+
+        A capture that finds the ring full waits on the device
+        (TF_FULL_WAIT) with its whole grid resident. That is right inside a
+        CUDA graph, where the host cannot pause a replay, but in eager code it
+        lets any host call that waits for the device (a synchronising copy,
+        cudaFree under allocator pressure, a pinned allocation) block while
+        the device waits for the staging engine. So before launching, the
+        host waits until the bytes launched and not yet released, plus this
+        reservation, leave room for one dead skip (the largest reservation):
+        the device then always finds space. The estimate uses the planned
+        payload lengths and the consumer's host-side release total; if it
+        stays blocked (the estimate drifted), it is re-based once on an
+        exact device snapshot."""
+        if need > self._max_need:
+            self._max_need = need
+        cap = self.ring.capacity
+        limit = cap - self._max_need - need  # in flight allowed before this one
+
+        def admitted() -> bool:
+            before = self._launched - self._released
+            return before <= 0 or before <= limit   # an empty ring fits anything
+
+        if admitted():
+            self._launched += need
+            return
+        import ctypes as C
+        lib = N.lib()
+        rel = C.c_uint64()
+        t0 = time.monotonic()
+        rebased = False
+        while True:
+            N.check(lib.tf_ring_host_released(self.ring.handle, C.byref(rel), None))
+            self._released = rel.value
+            if admitted():
+                break
+            self.exporter._check_bg()
+            waited = time.monotonic() - t0
+            if waited > 0.25 and not rebased:
+                # every launched capture has reserved once the producer
+                # stream is synchronised: occupancy is then exact (dead
+                # bytes count as in flight: conservative by at most a skip)
+                torch().cuda.current_stream(self.device).synchronize()
+                occ = self.ring.state().occupancy
+                N.check(lib.tf_ring_host_released(self.ring.handle, C.byref(rel), None))
+                self._released = rel.value
+                self._launched = self._released + occ
+                rebased = True
+                continue
+            if waited > self.wait_timeout:
+                from .errors import PayloadRingFull
+                raise PayloadRingFull(
+                    f"capture of {need} bytes: the consumer released nothing for "
+                    f"{waited:.0f} s (ring {cap} bytes)")
+            time.sleep(2e-5)
+        self._launched += need
+        self.gate_waits += 1
+        self.gate_wait_s += time.monotonic() - t0
 
 
 class _CompletenessRingView:

@@ -24,6 +24,14 @@ ap.add_argument("--n", type=int, default=24)
 ap.add_argument("--timeout", type=float, default=60.0)
 ap.add_argument("--ring-mib", type=int, default=2048)
 ap.add_argument("--sizes-mib", default="896,256")
+ap.add_argument("--default-stream", action="store_true",
+                help="launch on the legacy default stream (as HF eager code does)")
+ap.add_argument("--host-op", default="none",
+                choices=["none", "pin", "empty_cache", "malloc", "item", "sink"],
+                help="what the main thread does while the captures wait on the device: "
+                     "pin = pinned host allocations, empty_cache = cudaFree of cached "
+                     "blocks, malloc = new device allocations, item = a blocking D2H "
+                     "read on another stream, sink = a Python NullSink consumer thread")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -36,8 +44,12 @@ pipe = ExportPipeline(ring, DrainConfig(min_ready_entries=1, min_ready_bytes=1, 
 keep = torch.ones(B, dtype=torch.uint8, device=dev)
 sizes = [int(x) << 20 for x in args.sizes_mib.split(",")]
 xs = [torch.empty(n, dtype=torch.uint8, device=dev).random_() for n in sizes]
-s = torch.cuda.Stream()
-pipe.start(sink=None)
+s = torch.cuda.default_stream(dev) if args.default_stream else torch.cuda.Stream()
+if args.host_op == "sink":
+    from paper_2605_11093_b200.sinks import NullSink
+    pipe.start(sink=NullSink())
+else:
+    pipe.start(sink=None)
 done = threading.Event()
 t0 = time.perf_counter()
 
@@ -87,8 +99,28 @@ with torch.cuda.stream(s):
 ev = torch.cuda.Event()
 ev.record(s)
 deadline = time.perf_counter() + args.timeout
+other = torch.cuda.Stream()
+keepalive = []
+k = 0
 while not ev.query() and time.perf_counter() < deadline:
+    k += 1
+    if args.host_op == "pin":
+        keepalive.append(torch.empty(64 << 20, dtype=torch.uint8).pin_memory())
+        if len(keepalive) > 4:
+            keepalive.pop(0)
+    elif args.host_op == "empty_cache":
+        keepalive.append(torch.empty(256 << 20, dtype=torch.uint8, device=dev))
+        keepalive.clear()
+        torch.cuda.empty_cache()
+    elif args.host_op == "malloc":
+        keepalive.append(torch.empty((256 + k) << 20, dtype=torch.uint8, device=dev))
+        if len(keepalive) > 4:
+            keepalive.pop(0)
+    elif args.host_op == "item":
+        with torch.cuda.stream(other):
+            torch.ones(1, device=dev).sum().item()
     time.sleep(0.05)
+print(json.dumps({"host_op": args.host_op, "host_op_iterations": k}), flush=True)
 ok = ev.query()
 print(json.dumps({"captures_done": ok, "elapsed_s": time.perf_counter() - t0}), flush=True)
 if ok:
