@@ -862,6 +862,25 @@ def leg_overload(args, dist, dev, steps=12):
     def graph_of(obs=None):
         return Eager
 
+    def run(gr, obs=None, base_seq=0):
+        """`steps` back-to-back prefill steps; device ms per step and the
+        request-steps kept / dropped by the policy."""
+        kept = dropped = 0
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s_ in range(steps):
+            if obs is not None:
+                plan = obs.begin_step(batch, base_seq + s_)
+                kept += len(plan.kept_ids)
+                dropped += len(plan.dropped_ids)
+            gr.replay()
+            if obs is not None:
+                obs.end_step(stream)
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / steps, kept, dropped
+
     g0 = graph_of()
     run(g0)
     base, _, _ = run(g0)

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <pthread.h>
 #include <sched.h>
+#include <sys/mman.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
@@ -275,6 +276,10 @@ struct tf_stager {
   std::deque<Batch*> to_stage;
   std::deque<tf_paged_batch> out_q;
   std::vector<uint8_t*> paged_pool;
+  // page-out buffers of split (oversize) captures, kept for reuse: a fresh
+  // allocation of hundreds of MiB pays its page faults inside the copy
+  std::multimap<uint64_t, uint8_t*> oversize_pool;   // capacity -> buffer
+  std::map<uint8_t*, uint64_t> oversize_cap;         // buffer -> capacity
   uint32_t outstanding_paged = 0;
   uint64_t outstanding_handoff = 0;  // pinned buffers held by the consumer
   uint64_t max_split_bufs = 0;       // most chunk buffers one split capture took
@@ -381,6 +386,7 @@ extern "C" int tf_stager_destroy(tf_stager* st) {
   for (auto e : st->event_pool) cudaEventDestroy(e);
   for (auto p : st->bufs) cudaFreeHost(p);
   for (auto p : st->paged_pool) free(p);
+  for (auto& kv : st->oversize_pool) free(kv.second);
   if (st->stream) cudaStreamDestroy(st->stream);
   delete st;
   return TF_OK;
@@ -834,6 +840,38 @@ static void set_bg_error(tf_stager* st, int rc) {
   st->cv.notify_all();
 }
 
+// A page-out buffer for a split capture of `bytes` (caller holds st->mu):
+// the smallest cached one that fits, else a new 2 MiB-aligned allocation
+// advised for transparent huge pages.
+static uint8_t* oversize_alloc(tf_stager* st, uint64_t bytes) {
+  auto it = st->oversize_pool.lower_bound(bytes);
+  if (it != st->oversize_pool.end()) {
+    uint8_t* p = it->second;
+    st->oversize_pool.erase(it);
+    return p;
+  }
+  const uint64_t huge = uint64_t(2) << 20;
+  const uint64_t cap = (bytes + huge - 1) & ~(huge - 1);
+  uint8_t* p = (uint8_t*)aligned_alloc(huge, cap);
+  if (!p) return nullptr;
+  madvise(p, cap, MADV_HUGEPAGE);
+  st->oversize_cap[p] = cap;
+  return p;
+}
+
+// Back to the cache (at most kOversizeCached buffers), else freed.
+constexpr size_t kOversizeCached = 4;
+static void oversize_free(tf_stager* st, uint8_t* p) {
+  auto c = st->oversize_cap.find(p);
+  if (c == st->oversize_cap.end()) { free(p); return; }
+  if (st->oversize_pool.size() < kOversizeCached) {
+    st->oversize_pool.emplace(c->second, p);
+    return;
+  }
+  st->oversize_cap.erase(c);
+  free(p);
+}
+
 static uint8_t* paged_alloc(tf_stager* st) {  // caller holds st->mu
   if (!st->paged_pool.empty()) {
     uint8_t* p = st->paged_pool.back();
@@ -852,7 +890,8 @@ static void free_paged_batch(tf_stager* st, tf_paged_batch* b, bool to_pool) {
     if (st->outstanding_handoff) st->outstanding_handoff -= 1;
     st->cv.notify_all();
   } else if (b->payload) {
-    if (to_pool && !b->oversize) st->paged_pool.push_back((uint8_t*)b->payload);
+    if (b->oversize) oversize_free(st, (uint8_t*)b->payload);
+    else if (to_pool) st->paged_pool.push_back((uint8_t*)b->payload);
     else free(b->payload);
   }
   b->pinned_buffer = -1;
@@ -997,7 +1036,10 @@ static void stage_loop(tf_stager* st) {
     const bool split = !b->chunk_bufs.empty();
     st->stage_phase = 1;
     if (split) {
-      dst = (uint8_t*)aligned_alloc(4096, (b->bytes + 4095) & ~uint64_t(4095));
+      {
+        std::lock_guard<std::mutex> g(st->mu);
+        dst = oversize_alloc(st, b->bytes);
+      }
       if (!dst) {
         tf_set_error("pageable allocation of a split capture (%llu bytes) failed",
                      (unsigned long long)b->bytes);

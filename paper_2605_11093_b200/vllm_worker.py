@@ -208,7 +208,10 @@ class ObservedWorker(Worker):
                               max_wait=float(cfg.get("drain_wait", 2e-3)),
                               staging_buffer_size=int(cfg["staging_buffer_mib"]) << 20,
                               staging_buffer_count=int(cfg["staging_buffers"]),
-                              page_out="handoff"),
+                              page_out="handoff",
+                              # a prefill-heavy step (max_num_batched_tokens
+                              # rows of mlp_act) can exceed one buffer
+                              split_oversize=True),
             policy=policy, sink=self._tf_sink, device=self.local_rank,
             max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True,
             debug_row_bytes=dbg_rows)
