@@ -1216,9 +1216,50 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         // MODE_REDUCE: one warp per row, fp64 accumulation, f32 outputs
         constexpr int WI = Elem<IN_DT>::W;
         const int64_t H = P.row_elems;
-        double sum = 0.0, sq = 0.0;
-        float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
-        auto finish_row = [&](int64_t j) {
+        for (int64_t j = s_first; j < s_end; j += s_step) {
+          const uint8_t* src = row_src(P, row_of(j));
+          double sum = 0.0, sq = 0.0;
+          float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
+          if (VW == 8) {
+            const int64_t G8 = H / 8;
+            constexpr int NR = IN_DT == TF_F32 ? 2 : 1;
+            constexpr int RU = IN_DT == TF_F32 ? kUnroll / 2 : kUnroll;  // loads in flight
+            for (int64_t g0 = lane; g0 < G8; g0 += 32 * RU) {
+              uint4 raw[RU][NR];
+#pragma unroll
+              for (int u = 0; u < RU; ++u) {
+                const int64_t g = g0 + int64_t(u) * 32;
+                if (g < G8) {
+#pragma unroll
+                  for (int q = 0; q < NR; ++q) raw[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < RU; ++u) {
+                if (g0 + int64_t(u) * 32 < G8) {
+                  float f[8];
+                  cvt8<IN_DT>(raw[u], f);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    sum += (double)f[e];
+                    sq += (double)f[e] * (double)f[e];
+                    mn = fminf(mn, f[e]);
+                    mx = fmaxf(mx, f[e]);
+                    amax = fmaxf(amax, fabsf(f[e]));
+                  }
+                }
+              }
+            }
+          } else {
+            for (int64_t e = lane; e < H; e += 32) {
+              float x = load_elem<IN_DT>(src + e * WI);
+              sum += (double)x;
+              sq += (double)x * (double)x;
+              mn = fminf(mn, x);
+              mx = fmaxf(mx, x);
+              amax = fmaxf(amax, fabsf(x));
+            }
+          }
 #pragma unroll
           for (int d = 16; d > 0; d >>= 1) {
             sum += __shfl_xor_sync(0xffffffffu, sum, d);
@@ -1240,79 +1281,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
                 o[2] = mn;
                 o[3] = mx;
             }
-          }
-          sum = sq = 0.0;
-          mn = __int_as_float(0x7f800000);
-          mx = -__int_as_float(0x7f800000);
-          amax = 0.f;
-        };
-        if constexpr (VW == 8) {
-          // The warp's rows as one stream of (row, batch) items, a batch
-          // being RU 8-element groups per lane; the loads of the next item
-          // are issued before the current one is accumulated, so reads stay
-          // in flight across row boundaries. Each 8-group is summed in fp32
-          // (bf16/f16 inputs and their squares are exact in fp32; the
-          // partial's rounding is ~1e-7 relative) and accumulated in fp64.
-          const int64_t G8 = H / 8;
-          constexpr int NR = IN_DT == TF_F32 ? 2 : 1;
-          constexpr int RU = IN_DT == TF_F32 ? kUnroll / 2 : kUnroll;
-          const int64_t nb = (G8 + 32 * RU - 1) / (32 * RU);  // batches per row
-          uint4 cur[RU][NR], nxt[RU][NR];
-          auto load_item = [&](int64_t jj, int64_t bb, uint4 (&r)[RU][NR]) {
-            const uint8_t* src = row_src(P, row_of(jj));
-#pragma unroll
-            for (int u = 0; u < RU; ++u) {
-              const int64_t g = bb * 32 * RU + int64_t(u) * 32 + lane;
-              if (g < G8) {
-#pragma unroll
-                for (int q = 0; q < NR; ++q) r[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
-              }
-            }
-          };
-          int64_t j = s_first, b = 0;
-          if (j < s_end) load_item(j, 0, cur);
-          while (j < s_end) {
-            int64_t jn = j, bn = b + 1;
-            if (bn == nb) { bn = 0; jn = j + s_step; }
-            if (jn < s_end) load_item(jn, bn, nxt);
-#pragma unroll
-            for (int u = 0; u < RU; ++u) {
-              if (b * 32 * RU + int64_t(u) * 32 + lane < G8) {
-                float f[8];
-                cvt8<IN_DT>(cur[u], f);
-                float s8 = 0.f, q8 = 0.f;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  s8 += f[e];
-                  q8 = fmaf(f[e], f[e], q8);
-                  mn = fminf(mn, f[e]);
-                  mx = fmaxf(mx, f[e]);
-                  amax = fmaxf(amax, fabsf(f[e]));
-                }
-                sum += (double)s8;
-                sq += (double)q8;
-              }
-            }
-            if (bn == 0) finish_row(j);
-#pragma unroll
-            for (int u = 0; u < RU; ++u)
-#pragma unroll
-              for (int q = 0; q < NR; ++q) cur[u][q] = nxt[u][q];
-            j = jn;
-            b = bn;
-          }
-        } else {
-          for (int64_t j = s_first; j < s_end; j += s_step) {
-            const uint8_t* src = row_src(P, row_of(j));
-            for (int64_t e = lane; e < H; e += 32) {
-              float x = load_elem<IN_DT>(src + e * WI);
-              sum += (double)x;
-              sq += (double)x * (double)x;
-              mn = fminf(mn, x);
-              mx = fmaxf(mx, x);
-              amax = fmaxf(amax, fabsf(x));
-            }
-            finish_row(j);
           }
         }
       }
