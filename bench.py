@@ -663,12 +663,16 @@ def leg_model(args, dist, dev, model):
         run(2, step0)
         base, base_half = run(n, step0, halves=True)
         res = {"no_capture_ms": base, "no_capture_ms_second_half": base_half}
-        cases = [("resid", ("resid_post",), PolicyConfig()),
-                 ("resid_mlp", ("mlp_act", "resid_post"), PolicyConfig())]
+        cases = [("resid", ("resid_post",), PolicyConfig(), False),
+                 ("resid_mlp", ("mlp_act", "resid_post"), PolicyConfig(), False)]
         if mode == "graph":  # overload regime under the best-effort policy
             cases.append(("resid_mlp_best_effort", ("mlp_act", "resid_post"),
-                          PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT)))
-        for label, sites, policy in cases:
+                          PolicyConfig(mode=BEST_EFFORT, strategy=DROP_RECENT), False))
+            # captures on a side stream, overlapping the next layers
+            cases.append(("resid_overlap", ("resid_post",), PolicyConfig(), True))
+            cases.append(("resid_mlp_overlap", ("mlp_act", "resid_post"), PolicyConfig(),
+                          True))
+        for label, sites, policy, overlap in cases:
             log(f"model {mode} {label} (base {base:.1f} ms)")
             reg = llama_registry(cfg, sites)
             step_bytes = sum(reg.slice_bytes(h, T) for h in reg.enabled_ids()) * B
@@ -685,7 +689,7 @@ def leg_model(args, dist, dev, model):
                                              mode=args.staging, stage_threads=4,
                                              page_out=args.page_out),
                            policy=policy, sink=sink, device=dev.index,
-                           max_batch=B)
+                           max_batch=B, overlap=overlap)
             obs.exporter.copy_payloads = False
             obs.start()
             handles = attach_llama(model, obs, sites)
@@ -716,7 +720,7 @@ def leg_model(args, dist, dev, model):
                 "overhead_pct_incl_export_tail":
                     (t + t_tail * 1e3 / n - base) / base * 100.0,
                 "ring_bytes": ring_bytes, "steps": n,
-                "step_bytes": step_bytes, "policy": policy.mode,
+                "step_bytes": step_bytes, "policy": policy.mode, "overlap": overlap,
                 "stall_events": st.stall_events,
                 "dropped_request_steps": tally["dropped"],
                 "kept_request_steps": tally["kept"],

@@ -787,6 +787,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // capture wrote the producer snapshot). No-ops without the launch attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef TF_TRACE
+  // phase stamps start when the CTA may touch memory (a PDL-launched CTA
+  // can be resident long before that)
+  const uint64_t t_go = tid == 0 ? globaltimer() : 0;
+#endif
   // Issue the producer-snapshot and step loads first: their latency hides
   // behind the keep scan (step is consumed only by the publishing CTA).
   SnapRegs sr;
@@ -1319,7 +1324,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #ifdef TF_TRACE
     if (tid == 0 && blockIdx.x < kTrCtas) {
       const int slot = int(sh.fast_seq % kTrLaunches);
-      g_stamp[slot][blockIdx.x][0] = t_entry;
+      g_stamp[slot][blockIdx.x][0] = t_go;
       g_stamp[slot][blockIdx.x][1] = t_plan;
       g_stamp[slot][blockIdx.x][2] = globaltimer();
       g_stamp[slot][blockIdx.x][3] = t_scan;
@@ -1338,7 +1343,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     {
       const int slot = sh.fast ? int(sh.fast_seq % kTrLaunches) : kTrLaunches - 1;
       if (blockIdx.x < kTrCtas) {
-        g_stamp[slot][blockIdx.x][0] = t_entry;
+        g_stamp[slot][blockIdx.x][0] = t_go;
         g_stamp[slot][blockIdx.x][1] = t_plan;
         g_stamp[slot][blockIdx.x][2] = globaltimer();
         g_stamp[slot][blockIdx.x][3] = t_scan;

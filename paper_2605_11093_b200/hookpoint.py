@@ -78,7 +78,7 @@ class Observer:
                  sampled_hooks: frozenset = frozenset(),
                  rank_coords: tuple = (0, 0), wait_timeout: float = 60.0,
                  flat_rows: int = 0, persistent: bool = False,
-                 debug_row_bytes: dict | None = None):
+                 debug_row_bytes: dict | None = None, overlap: bool = False):
         t = torch()
         self.registry = registry
         self.policy = policy or PolicyConfig()
@@ -157,6 +157,16 @@ class Observer:
         self._recording = False
         self.gate_waits = 0
         self.gate_wait_s = 0.0
+        # overlap=True: capture kernels run on a side stream forked from the
+        # producer stream at each HookPoint, so they overlap the model's next
+        # kernels instead of sitting between them; join() (at end_step, or
+        # an integration's join hook before an activation is mutated in
+        # place) makes the producer stream wait for them. One side stream:
+        # the captures stay serialised among themselves, as the producer
+        # snapshot protocol requires.
+        self.overlap = overlap
+        self.side_stream = t.cuda.Stream(device=dev) if overlap else None
+        self._forked = False
 
     # -- session -----------------------------------------------------------
 
@@ -175,8 +185,21 @@ class Observer:
         self.ring.close()
 
     def flush(self, timeout: float = 120.0) -> None:
+        self.join()
         self.ring.sync()
         self.exporter.flush(timeout)
+
+    def join(self, stream=None) -> None:
+        """Make the producer stream wait for the side-stream captures
+        launched since the last join (overlap mode; a no-op otherwise).
+        Must run before a captured activation is modified in place, and
+        inside a CUDA-graph capture before the capture ends."""
+        if not self._forked:
+            return
+        t = torch()
+        cur = stream if stream is not None else t.cuda.current_stream(self.device)
+        cur.wait_stream(self.side_stream)
+        self._forked = False
 
     # -- per step --------------------------------------------------------------
 
@@ -379,6 +402,7 @@ class Observer:
         return self._batch[0].token_start if self._batch else 0
 
     def end_step(self, stream=None) -> None:
+        self.join(stream)
         self.ring.note_launch(stream)
         self.active = self.persistent
 
@@ -458,7 +482,17 @@ class Observer:
             q = self._need.get(hook.name)
             if q:
                 self._admit(q.pop())
-        launch_capture(self.ring, args, stream)
+        if self.overlap:
+            t = torch()
+            cur = stream if stream is not None else t.cuda.current_stream(self.device)
+            side = self.side_stream
+            side.wait_stream(cur)         # the source rows and keep uploads first
+            launch_capture(self.ring, args, side)
+            if isinstance(x, t.Tensor):
+                x.record_stream(side)     # no reuse of the rows before the copy
+            self._forked = True
+        else:
+            launch_capture(self.ring, args, stream)
         self.launches += 1
         dbg = self.debug_clone.get(hook_id)
         if dbg is not None:
@@ -657,6 +691,34 @@ def _capture_fake(x, token, observer, hook_id) -> None:
     return None
 
 
+@torch().library.custom_op(
+    "ring2::join", mutates_args=("token",),
+    schema="(Tensor(a!) token, int observer) -> ()")
+def _join_op(token, observer):
+    ref = _OBSERVERS[observer] if 0 <= observer < len(_OBSERVERS) else None
+    obs = ref() if ref is not None else None
+    if obs is not None:
+        obs.join()
+
+
+@_join_op.register_fake
+def _join_fake(token, observer) -> None:
+    return None
+
+
+def join_point(observer: Observer) -> None:
+    """Call from model code (or a hook) where the overlap-mode captures must
+    be complete: traced as the ``ring2::join`` custom op under torch.compile,
+    a direct ``Observer.join`` otherwise."""
+    if observer is None or not observer.overlap:
+        return
+    t = torch()
+    if t.compiler.is_compiling():
+        t.ops.ring2.join(observer.token, observer.index)
+    else:
+        observer.join()
+
+
 def total_step_bytes(registry: HookRegistry, batch) -> int:
     from .policy import estimate_step_bytes
     return sum(estimate_step_bytes(registry, batch))
@@ -666,5 +728,5 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-__all__ = ["HookPoint", "Observer", "TokenSampler", "total_step_bytes",
+__all__ = ["HookPoint", "Observer", "TokenSampler", "join_point", "total_step_bytes",
            "ceil_div"]

@@ -23,7 +23,7 @@ execution order: attn sites, then mlp_act, then resid_post.
 
 from __future__ import annotations
 
-from .hookpoint import HookPoint, Observer
+from .hookpoint import HookPoint, Observer, join_point
 from .hooks import DType, HookSpec, ModelSpec, install_hooks
 
 SITE_ORDER = ("k_slice", "v_slice", "k_cache", "v_cache", "attn_pattern",
@@ -144,6 +144,11 @@ def attach_llama(model, observer: Observer | None, sites) -> list:
         if "resid_post" in hps:
             handles.append(layer.register_forward_hook(
                 lambda m, a, out, hp=hps["resid_post"]: (hp(_first(out)), None)[1]))
+    if observer is not None and observer.overlap:
+        # overlap mode: HF writes no captured activation in place, so one
+        # join after the last layer suffices (inside a recorded graph too)
+        handles.append(inner.norm.register_forward_hook(
+            lambda m, a, out: (join_point(observer), None)[1]))
     return handles
 
 

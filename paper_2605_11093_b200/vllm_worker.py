@@ -45,7 +45,7 @@ import time
 from vllm.v1.worker.gpu_worker import Worker
 
 from .exporter import DrainConfig
-from .hookpoint import HookPoint, Observer
+from .hookpoint import HookPoint, Observer, join_point
 from .hooks import DType, HookSpec, ModelSpec, install_hooks
 from .policy import BEST_EFFORT, COMPLETENESS, DROP_RECENT, PolicyConfig, StepRequest
 from .rings import RingConfig
@@ -78,6 +78,15 @@ def attach_vllm_llama(model, observer: Observer, sites) -> list:
         model.add_module("hookpoint_" + name.replace("[", "_").replace("]", ""), hp)
         return hp
 
+    if observer.overlap:
+        # overlap mode: side-stream captures must be complete before vLLM's
+        # fused add+RMSNorm rewrites the residual in place (the layer's
+        # post-attention norm) and before each CUDA-graph piece ends (vLLM
+        # splits its graphs at the attention op): join right before every
+        # attention call, and after the last capture at the final norm
+        for layer in layers:
+            handles.append(layer.self_attn.attn.register_forward_pre_hook(
+                lambda m, args: (join_point(observer), None)[1]))
     for L, layer in enumerate(layers):
         if "mlp_act" in sites:
             hp = add(f"mlp_act[{L}]")
@@ -94,6 +103,9 @@ def attach_vllm_llama(model, observer: Observer, sites) -> list:
         handles.append(inner.norm.register_forward_hook(
             lambda m, a, out, hp=hp: (hp(out[1]) if isinstance(out, tuple)
                                       else None, None)[1]))
+    if observer.overlap:
+        handles.append(inner.norm.register_forward_hook(
+            lambda m, a, out: (join_point(observer), None)[1]))
     return handles
 
 
@@ -149,6 +161,15 @@ def _clone_hooks(model, store, step_of, sites) -> list:
 
     def keep(name, x):
         store.append((step_of(), name, x.detach().to("cpu", copy=True)))
+    if observer.overlap:
+        # overlap mode: side-stream captures must be complete before vLLM's
+        # fused add+RMSNorm rewrites the residual in place (the layer's
+        # post-attention norm) and before each CUDA-graph piece ends (vLLM
+        # splits its graphs at the attention op): join right before every
+        # attention call, and after the last capture at the final norm
+        for layer in layers:
+            handles.append(layer.self_attn.attn.register_forward_pre_hook(
+                lambda m, args: (join_point(observer), None)[1]))
     for L, layer in enumerate(layers):
         if "mlp_act" in sites:
             hs.append(layer.mlp.down_proj.register_forward_pre_hook(
@@ -214,7 +235,7 @@ class ObservedWorker(Worker):
                               split_oversize=True),
             policy=policy, sink=self._tf_sink, device=self.local_rank,
             max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True,
-            debug_row_bytes=dbg_rows)
+            debug_row_bytes=dbg_rows, overlap=bool(cfg.get("overlap", False)))
         # records that outlive the batch (ListSink) must own their bytes
         obs.exporter.copy_payloads = cfg.get("sink") == "list"
         obs.start()

@@ -31,6 +31,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--mode", choices=["eager", "graph"], default="eager")
 ap.add_argument("--requests", type=int, default=13)
 ap.add_argument("--output-len", type=int, default=12)
+ap.add_argument("--overlap", action="store_true",
+                help="captures on the observer's side stream (Observer(overlap=True))")
 args = ap.parse_args()
 
 d = tempfile.mkdtemp(prefix="tiny_llama_")
@@ -44,7 +46,8 @@ json.dump({"architectures": ["LlamaForCausalLM"], "model_type": "llama",
 os.environ["TF_VLLM_OBSERVER"] = json.dumps({
     "sites": ["resid_post", "mlp_act"], "ring_bytes": 256 << 20, "meta_slots": 4096,
     "policy": "completeness", "sink": "list", "staging_buffer_mib": 16,
-    "debug_clone": args.mode == "eager", "debug_graph_clone": args.mode == "graph"})
+    "debug_clone": args.mode == "eager", "debug_graph_clone": args.mode == "graph",
+    "overlap": args.overlap})
 
 import torch  # noqa: E402
 from vllm import LLM, SamplingParams  # noqa: E402
@@ -77,7 +80,8 @@ for h, s, rid, shape, payload in recs:
 missing = [k for k in expected if k not in got]
 extra = [k for k in got if k not in expected]
 rows_bad = [k for k, (shape, _) in got.items() if k in expected and shape[0] != expected[k]]
-out = {"mode": args.mode, "records": len(recs), "expected": len(expected),
+out = {"mode": args.mode, "overlap": args.overlap, "records": len(recs),
+       "expected": len(expected),
        "hooks": len(hooks), "steps": len(layouts), "missing": len(missing),
        "extra": len(extra), "duplicates": dup, "row_count_mismatch": len(rows_bad)}
 # every record against its request's rows of the reference copy

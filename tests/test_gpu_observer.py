@@ -478,3 +478,65 @@ def test_eager_oversize_captures_with_blocking_host_calls():
     assert st.drops == 0 and not (st.device_errors & 0x2)
     assert got == want
     assert obs.gate_waits > 0
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_overlap_side_stream_captures_before_in_place_update(graph):
+    """overlap=True: capture kernels run on a side stream forked at each
+    HookPoint. Here each captured activation is overwritten in place right
+    after a join point (as vLLM's fused add+RMSNorm rewrites the residual),
+    eagerly and inside a replayed CUDA graph: records hold the values before
+    the update, bit for bit, over fresh inputs every step."""
+    from paper_2605_11093_b200.hookpoint import join_point
+    B, T, H, L = 4, 32, 512, 3
+    reg = install_hooks(ModelSpec(L, H), [HookSpec(
+        "resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True)])
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(16 << 20, 256), sink=sink, max_batch=B,
+                   drain=DrainConfig(min_ready_entries=1), overlap=True)
+    obs.start()
+    hps = [HookPoint(f"resid[{i}]", obs) for i in range(L)]
+    x = torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda")
+    lin = torch.nn.Linear(H, H, device="cuda", dtype=torch.bfloat16)
+    resid = torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda")
+    snaps = [torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+
+    def body():
+        resid.copy_(x)
+        for i in range(L):
+            resid.add_(lin(resid))        # the residual after layer i
+            snaps[i].copy_(resid)         # what the capture must see
+            hps[i](resid)                 # forked capture
+            h = lin(resid)                # work the capture overlaps
+            join_point(obs)               # before the in-place update
+            resid.mul_(0.5).add_(h)       # in place, as a fused add-norm
+
+    if graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            body()
+        torch.cuda.current_stream().wait_stream(s)
+        obs.flush()
+        sink.records.clear()
+        g = torch.cuda.CUDAGraph()
+        with obs.graph_capture(), torch.cuda.graph(g):
+            body()
+        run = g.replay
+    else:
+        run = body
+    expected = []
+    for step in range(4):
+        x.copy_(torch.randn(B, T, H, dtype=torch.bfloat16))
+        obs.begin_step([StepRequest(i, i, "p", T, 0) for i in range(B)], 20 + step)
+        run()
+        obs.end_step()
+        torch.cuda.synchronize()
+        for i in range(L):
+            for b in range(B):
+                expected.append((b, f"resid[{i}]", 20 + step,
+                                 snaps[i][b].contiguous().view(torch.uint8).cpu().numpy().tobytes()))
+    obs.flush()
+    obs.close()
+    got = [(r.request_id, r.hook_name, r.step_seq, bytes(r.payload)) for r in sink.records]
+    assert sorted(got) == sorted(expected)
