@@ -186,6 +186,8 @@ class Observer:
 
     def flush(self, timeout: float = 120.0) -> None:
         self.join()
+        if self.side_stream is not None:
+            self.side_stream.synchronize()  # every side-stream capture has published
         self.ring.sync()
         self.exporter.flush(timeout)
 
@@ -546,6 +548,8 @@ class Observer:
                 # stream is synchronised: occupancy is then exact (dead
                 # bytes count as in flight: conservative by at most a skip)
                 torch().cuda.current_stream(self.device).synchronize()
+                if self.side_stream is not None:
+                    self.side_stream.synchronize()
                 occ = self.ring.state().occupancy
                 N.check(lib.tf_ring_host_released(self.ring.handle, C.byref(rel), None))
                 self._released = rel.value
