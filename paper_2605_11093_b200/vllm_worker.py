@@ -161,15 +161,6 @@ def _clone_hooks(model, store, step_of, sites) -> list:
 
     def keep(name, x):
         store.append((step_of(), name, x.detach().to("cpu", copy=True)))
-    if observer.overlap:
-        # overlap mode: side-stream captures must be complete before vLLM's
-        # fused add+RMSNorm rewrites the residual in place (the layer's
-        # post-attention norm) and before each CUDA-graph piece ends (vLLM
-        # splits its graphs at the attention op): join right before every
-        # attention call, and after the last capture at the final norm
-        for layer in layers:
-            handles.append(layer.self_attn.attn.register_forward_pre_hook(
-                lambda m, args: (join_point(observer), None)[1]))
     for L, layer in enumerate(layers):
         if "mlp_act" in sites:
             hs.append(layer.mlp.down_proj.register_forward_pre_hook(
