@@ -314,6 +314,16 @@ __device__ __forceinline__ void store8(uint8_t* p, const float* f) {
 // ---------------------------------------------------------------------------
 // capture kernel
 // ---------------------------------------------------------------------------
+// Division by a launch-constant divisor as a multiply-high and a shift
+// (the divisors -- segments per row, rows per keep unit, rows per outer
+// index, copy CTAs -- are known on the host at launch; ncu attributed ~25 %
+// of a decode-size capture's instructions to the divider). q = n / d for
+// n < 2^31: mul = ceil(2^p / d) with p = 31 + ceil(log2 d), q = umulhi(n, mul)
+// >> (p - 32); d == 1 is mul == 0.
+struct FastDiv {
+  uint32_t d, mul, shr;
+};
+
 struct CapParams {
   const uint8_t* src;
   int64_t outer, mid, row_bytes, s_outer, s_mid;
@@ -334,6 +344,9 @@ struct CapParams {
   DevCtl* ctl;
   uint64_t timeout_ns;
   uint8_t* done_flags;        // mapped host memory, kMaxFlagCtas per slot
+  // launch-constant divisors (set_fastdiv); fd_ok: every dividend < 2^31
+  FastDiv fd_spr, fd_rpu, fd_mid, fd_cg;
+  uint32_t fd_ok;
 };
 
 enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
@@ -751,8 +764,15 @@ __device__ __forceinline__ int64_t qdiv(int64_t a, int64_t b) {
   return a / b;
 }
 
+// a / b where b is the divisor `f` was built for (fast path when P.fd_ok)
+__device__ __forceinline__ int64_t fdiv(const CapParams& P, int64_t a, const FastDiv& f,
+                                        int64_t b) {
+  if (P.fd_ok) return f.mul ? int64_t(__umulhi(uint32_t(a), f.mul) >> f.shr) : a;
+  return qdiv(a, b);
+}
+
 __device__ __forceinline__ const uint8_t* row_src(const CapParams& P, int64_t row) {
-  int64_t o = qdiv(row, P.mid);
+  int64_t o = fdiv(P, row, P.fd_mid, P.mid);
   int64_t m = row - o * P.mid;
   return P.src + o * P.s_outer + m * P.s_mid;
 }
@@ -836,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       // (TF_SPEC_WARP0=0: warp 0, which runs the plan, skips the speculative
       // load so its memory queue stays empty; A/B builds)
       if (cb >= 0 && (TF_SPEC_WARP0 || warp != 0) && s0 < U * P.rpu * spr0) {
-        const int64_t j0 = qdiv(s0, spr0);
+        const int64_t j0 = fdiv(P, s0, P.fd_spr, spr0);
         const int64_t k0 = (s0 - j0 * spr0) * kSeg;
         const int64_t k1 = imin64(k0 + kSeg, P.words_per_row);
         const uint8_t* src = row_src(P, j0);
@@ -855,7 +875,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           for (int t = 0; t < kSmemSpec; ++t) {
             const int64_t sn = s0 + (t + 1) * sstep;
             if (sn < all) {
-              const int64_t jn = qdiv(sn, spr0);
+              const int64_t jn = fdiv(P, sn, P.fd_spr, spr0);
               const int64_t kn0 = (sn - jn * spr0) * kSeg;
               const int64_t kn1 = imin64(kn0 + kSeg, P.words_per_row);
               const uint8_t* srcn = row_src(P, jn);
@@ -988,14 +1008,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     spr = (P.words_per_row + kSeg - 1) / kSeg;
     items = packed ? qdiv((int64_t)n_rows + rps - 1, rps) : (int64_t)n_rows * spr;
   }
-  const int64_t chunk = qdiv(items + cg - 1, cg);
+  const int64_t chunk = fdiv(P, items + cg - 1, P.fd_cg, cg);
   const int64_t i0 = cb < 0 ? items : imin64(int64_t(cb) * chunk, items);
   const int64_t i1 = imin64(i0 + chunk, items);
-  const int64_t j_lo = qdiv(i0, spr);
-  const int64_t r_lo = qdiv(j_lo, P.rpu);
+  const int64_t j_lo = fdiv(P, i0, P.fd_spr, spr);
+  const int64_t r_lo = fdiv(P, j_lo, P.fd_rpu, P.rpu);
   const int64_t tbase = small ? 0 : r_lo;  // rank of sh.table[0]
   if (P.keep && !small && i0 < i1) {
-    const int64_t r_hi = qdiv(qdiv(i1 - 1, spr), P.rpu);
+    const int64_t r_hi = fdiv(P, fdiv(P, i1 - 1, P.fd_spr, spr), P.fd_rpu, P.rpu);
     // rank -> unit table for the ranks this CTA touches
     if ((int64_t)mybase <= r_hi && (int64_t)(mybase + mycnt) > r_lo) {
       int64_t rank = mybase;
@@ -1053,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     return;
   }
   auto row_of = [&](int64_t j) -> int64_t {
-    int64_t r = qdiv(j, P.rpu);
+    int64_t r = fdiv(P, j, P.fd_rpu, P.rpu);
     int64_t sub = j - r * P.rpu;
     int64_t unit = P.keep ? (int64_t)sh.table[r - tbase] : r;
     return unit * P.rpu + sub;
@@ -1103,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     int64_t s = s_first;
     int64_t k0 = 0, k1 = 0, j = 0;
     if (s < s_end) {
-      j = qdiv(s, spr);
+      j = fdiv(P, s, P.fd_spr, spr);
       k0 = (s - j * spr) * kSeg;
       k1 = imin64(k0 + kSeg, wpr);
       if (!(spec_s == s && prefix)) {
@@ -1143,7 +1163,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         s += s_step;
         ++it;
         if (s >= s_end) break;
-        j = qdiv(s, spr);
+        j = fdiv(P, s, P.fd_spr, spr);
         k0 = (s - j * spr) * kSeg;
         k1 = imin64(k0 + kSeg, wpr);
         if (smem_ok && it <= kSmemSpec) {
@@ -1183,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         constexpr int WI = Elem<IN_DT>::W, WO = Elem<OUT_DT>::W;
         const int64_t wpr = P.words_per_row;
         for (int64_t s = s_first; s < s_end; s += s_step) {
-          const int64_t j = s / spr;
+          const int64_t j = fdiv(P, s, P.fd_spr, spr);
           const int64_t k0 = (s - j * spr) * kSeg;
           const int64_t k1 = imin64(k0 + kSeg, wpr);
           const uint8_t* src = row_src(P, row_of(j));
@@ -2032,8 +2052,36 @@ static bool pdl_enabled() {
   return on;
 }
 
+static FastDiv make_fastdiv(uint64_t d) {
+  FastDiv f{uint32_t(d), 0u, 0u};
+  if (d <= 1) return f;
+  int l = 0;
+  while ((uint64_t(1) << l) < d) ++l;  // ceil(log2 d)
+  const int p = 31 + l;
+  f.mul = uint32_t(((uint64_t(1) << p) + d - 1) / d);
+  f.shr = uint32_t(p - 32);
+  return f;
+}
+
+// The kernel's launch-constant divisors (its spr, rpu, mid and copy-CTA
+// count) and whether every dividend it divides stays below 2^31.
+template <int MODE>
+static void set_fastdiv(CapParams& P, int grid) {
+  const int64_t spr = MODE == MODE_REDUCE ? 1 : (P.words_per_row + kSeg - 1) / kSeg;
+  const uint64_t rows = uint64_t(P.outer) * uint64_t(P.mid);
+  const uint64_t lim = uint64_t(1) << 31;
+  P.fd_ok = rows < lim && uint64_t(spr) < lim && rows * uint64_t(spr) + uint64_t(grid) < lim &&
+            uint64_t(P.mid) < lim && uint64_t(P.rpu) < lim;
+  P.fd_spr = make_fastdiv(uint64_t(spr));
+  P.fd_rpu = make_fastdiv(uint64_t(P.rpu));
+  P.fd_mid = make_fastdiv(uint64_t(P.mid));
+  P.fd_cg = make_fastdiv(uint64_t(grid));
+}
+
 template <int MODE, int VW, int IN, int OUT>
-static int launch(const CapParams& P, int grid, cudaStream_t s) {
+static int launch(const CapParams& P0, int grid, cudaStream_t s) {
+  CapParams P = P0;
+  set_fastdiv<MODE>(P, grid);
   // (the >48 KiB opt-in is set once per device in tf_ring_create, outside
   // any stream capture)
   constexpr int smem = (MODE == MODE_COPY && VW == 16 && kSmemSpec > 0) ? kSpecSmemBytes : 0;
