@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--ref-procs", type=int, default=0,
+                   help="reference arm: replica processes, one per host core "
+                        "(0 = every core in the affinity mask; 1 = single core)")
     p.add_argument("--batch", type=int, default=8)
     p.add_argument("--seq", type=int, default=512)
     p.add_argument("--staging", default="copy-engine",
@@ -1269,6 +1272,15 @@ def cpu_baseline(B, T, budget_s=12.0):
         threaded = run_threaded_sample(B, T)
     except Exception as exc:  # report, never fail the bench on the baseline
         threaded = {"error": repr(exc)[:200]}
+    try:  # every host core as an independent reference replica (--impl reference)
+        procs = len(prev)
+        rate, res = run_reference_procs(B, T, 2, 1, procs)
+        all_cores = {"value": rate, "unit": UNIT, "cores": procs,
+                     "sample": f"{procs} processes x 2 steps of 2 layers x "
+                               "(resid_post+mlp_act), one process per core, "
+                               "sum of per-process rates"}
+    except Exception as exc:
+        all_cores = {"error": repr(exc)[:200]}
     return {"value": total / dt / 1e9 if dt else None, "unit": UNIT,
             "cores": cores, "kind": kind,
             "sample": f"{n} samples x (2 layers x resid_post+mlp_act, "
@@ -1276,13 +1288,83 @@ def cpu_baseline(B, T, budget_s=12.0):
                       f"through capture()+ExportPipeline->NullSink, "
                       f"single-threaded Python (GIL) pinned to CPU {cpu}, {dt:.1f}s",
             "host": host,
-            "run_threaded": threaded}
+            "run_threaded": threaded,
+            "all_cores": all_cores}
+
+
+def _ref_worker(B, T, steps, warmup, cpu, barrier, q):
+    """One reference replica pinned to one host core (spawned process)."""
+    try:
+        os.sched_setaffinity(0, {cpu})
+        for _ in range(warmup):
+            reference_sample(1, B, T)
+        barrier.wait(600)
+        total, busy, kind = 0, 0.0, None
+        for _ in range(steps):
+            kind, b, t = reference_sample(2, B, T)
+            total += b
+            busy += t
+        q.put({"cpu": cpu, "kind": kind, "bytes": total, "busy_s": busy})
+    except BaseException as exc:  # reported by the parent
+        q.put({"cpu": cpu, "error": repr(exc)[:300]})
+
+
+def run_reference_procs(B, T, steps, warmup, procs):
+    """The reference is pure Python (GIL-bound): its path uses every host
+    core only as independent replicas, one process per core, each running
+    the same bounded samples concurrently. Aggregate = sum of the per-process
+    rates over their timed regions."""
+    import multiprocessing as mp
+    cpus = sorted(os.sched_getaffinity(0))[:procs]
+    ctx = mp.get_context("spawn")
+    q, barrier = ctx.Queue(), ctx.Barrier(len(cpus))
+    ps = [ctx.Process(target=_ref_worker, args=(B, T, steps, warmup, c, barrier, q))
+          for c in cpus]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=1800) for _ in ps]
+    for p in ps:
+        p.join(60)
+    bad = [r for r in res if "error" in r]
+    if bad:
+        raise RuntimeError(f"reference replica failed: {bad[0]}")
+    rate = sum(r["bytes"] / r["busy_s"] for r in res) / 1e9
+    return rate, res
 
 
 def run_reference(args, dist):
     if dist.rank != 0:
         return
     B, T = args.batch, args.seq
+    procs = args.ref_procs or len(os.sched_getaffinity(0))
+    if procs > 1:
+        log(f"reference arm: {procs} processes")
+        value, res = run_reference_procs(B, T, args.steps, args.warmup, procs)
+        kind = res[0]["kind"]
+        dt = max(r["busy_s"] for r in res)
+        total = sum(r["bytes"] for r in res)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": config_block(args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs,
+                             "kind": kind,
+                             "sample": f"{procs} processes, one per host core, each "
+                                       f"{args.steps} steps of 2 layers x "
+                                       f"(resid_post+mlp_act) {B}x{T} bf16 through "
+                                       "the reference capture()+ExportPipeline->"
+                                       f"NullSink ({total / GiB:.1f} GiB in all); "
+                                       "value = sum of per-process rates",
+                             "per_process_gbs": [round(r["bytes"] / r["busy_s"] / 1e9, 4)
+                                                 for r in res]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     for _ in range(args.warmup):
         reference_sample(1, B, T)
     total, dt, kind = 0, 0.0, None
