@@ -777,7 +777,11 @@ __device__ __forceinline__ const uint8_t* row_src(const CapParams& P, int64_t ro
   return P.src + o * P.s_outer + m * P.s_mid;
 }
 
-template <int MODE, int VW, int IN_DT, int OUT_DT>
+// SS: shared-memory speculative segments per warp (COPY/16). They only pay
+// off once the grid is capped and warps own several segments; below that
+// (captures up to ~4.6 MiB) the launch uses SS = 0 and no dynamic shared
+// memory (decode-size captures 0.34 us faster, profiles/r02/ablation_*).
+template <int MODE, int VW, int IN_DT, int OUT_DT, int SS = kSmemSpec>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams P) {
   __shared__ CapShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -866,13 +870,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           if (k < k1) v[i] = ld_stream<VW>(src + k * VW);
         }
         spec_s = s0;
-        if constexpr (VW == 16 && kSmemSpec > 0) {
+        if constexpr (VW == 16 && SS > 0) {
           // the warp's next segments of the grid-interleaved order, into its
           // shared-memory slots (each lane later reads back its own words)
           const int64_t sstep = int64_t(cg) * kWarps;
           const int64_t all = U * P.rpu * spr0;
 #pragma unroll
-          for (int t = 0; t < kSmemSpec; ++t) {
+          for (int t = 0; t < SS; ++t) {
             const int64_t sn = s0 + (t + 1) * sstep;
             if (sn < all) {
               const int64_t jn = fdiv(P, sn, P.fd_spr, spr0);
@@ -920,8 +924,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     if (kbyte) sh.table[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)tid;
     K = tot;
     // a prefix of ones (e.g. a graph-padded token layout) keeps the identity
-    // row map, so the speculative segments stay valid
-    prefix = __syncthreads_and(tid >= U || ((kbyte != 0) == (uint32_t(tid) < tot))) != 0;
+    // row map, so the speculative segments stay valid; the block-wide AND is
+    // taken at the table barrier below (one barrier fewer on this path)
+    prefix = tid >= U || ((kbyte != 0) == (uint32_t(tid) < tot));
     TSTAMP(t_scan);
   } else if (P.keep) {
     int64_t per = (U + kThreads - 1) / kThreads;
@@ -1032,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
       }
     }
   }
-  __syncthreads();
+  prefix = __syncthreads_and(prefix) != 0;  // (uniform unless the ballot path ran)
   TSTAMP(t_table);
   if (sh.flagmode && blockIdx.x == 0 && sh.publish && warp == 0 && lane < 8)
     sh.slot[lane] = sh.desc[lane];  // early post; the host waits for the flags
@@ -1149,7 +1154,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
 #endif
     // the shared-memory speculation holds iff the register one does (same
     // identity map, same interleaved order)
-    const bool smem_ok = VW == 16 && kSmemSpec > 0 && spec_s == s && prefix;
+    const bool smem_ok = VW == 16 && SS > 0 && spec_s == s && prefix;
     if (sh.status == TF_OK && s < s_end) {
       uint8_t* dst_base = P.payload + sh.off;
       int it = 0;
@@ -1166,8 +1171,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         j = fdiv(P, s, P.fd_spr, spr);
         k0 = (s - j * spr) * kSeg;
         k1 = imin64(k0 + kSeg, wpr);
-        if (smem_ok && it <= kSmemSpec) {
-          if constexpr (VW == 16 && kSmemSpec > 0) {
+        if (smem_ok && it <= SS) {
+          if constexpr (VW == 16 && SS > 0) {
             cpa_wait_all();
             const uint4* slot = spec_smem + (size_t(it - 1) * kWarps + warp) * kSeg;
 #pragma unroll
@@ -1186,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         }
       }
     }
-    if constexpr (VW == 16 && kSmemSpec > 0) cpa_wait_all();  // no copy left in flight
+    if constexpr (VW == 16 && SS > 0) cpa_wait_all();  // no copy left in flight
    }
   } else {
     if (tid == 0 && !fast) {
@@ -2078,13 +2083,13 @@ static void set_fastdiv(CapParams& P, int grid) {
   P.fd_cg = make_fastdiv(uint64_t(grid));
 }
 
-template <int MODE, int VW, int IN, int OUT>
+template <int MODE, int VW, int IN, int OUT, int SS = kSmemSpec>
 static int launch(const CapParams& P0, int grid, cudaStream_t s) {
   CapParams P = P0;
   set_fastdiv<MODE>(P, grid);
   // (the >48 KiB opt-in is set once per device in tf_ring_create, outside
   // any stream capture)
-  constexpr int smem = (MODE == MODE_COPY && VW == 16 && kSmemSpec > 0) ? kSpecSmemBytes : 0;
+  constexpr int smem = (MODE == MODE_COPY && VW == 16 && SS > 0) ? SS * 8 * kSeg * 16 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid + kCtl);  // (+ the controller CTA in controller builds)
   cfg.blockDim = dim3(kThreads);
@@ -2095,7 +2100,7 @@ static int launch(const CapParams& P0, int grid, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, capture_kernel<MODE, VW, IN, OUT>, P);
+  cudaLaunchKernelEx(&cfg, capture_kernel<MODE, VW, IN, OUT, SS>, P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     tf_set_error("capture launch: %s", cudaGetErrorString(e));
@@ -2259,7 +2264,12 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
     }
 #endif
     switch (vw) {
-      case 16: return launch<MODE_COPY, 16, 0, 0>(P, grid, s);
+      case 16:
+        // below the grid cap every warp owns at most one segment: no
+        // shared-memory speculation, no dynamic shared memory
+        if (grid_bytes < int(uint64_t(sm_count) * kCtasPerSm * waves - kCtl))
+          return launch<MODE_COPY, 16, 0, 0, 0>(P, grid, s);
+        return launch<MODE_COPY, 16, 0, 0>(P, grid, s);
       case 8: return launch<MODE_COPY, 8, 0, 0>(P, grid, s);
       case 4: return launch<MODE_COPY, 4, 0, 0>(P, grid, s);
       case 2: return launch<MODE_COPY, 2, 0, 0>(P, grid, s);
