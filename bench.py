@@ -352,13 +352,13 @@ def leg_value(args, dist, dev):
         for k, x in enumerate((r, m)):
             src = RowSource(x.data_ptr(), B, T, x.shape[-1] * 2, x.stride(0) * 2,
                             x.shape[-1] * 2, x)
-            cap_args.append((capture_args(src, hook_id=2 * L + k,
+            cap_args.append((capture_args(src, hook_id=2 * L + k, sealed=True,
                                           keep_ptr=keep.data_ptr(),
                                           keep_per_outer=True, step_seq=0,
                                           full="wait"), x.numel() * 2))
     n_caps = len(cap_args)
 
-    def run_step(step, events=None):
+    def run_step(step, events=None, seal=True):
         for i, (a, nbytes) in enumerate(cap_args):
             a.step_seq = step
             if events is not None:
@@ -366,6 +366,8 @@ def leg_value(args, dist, dev):
             launch_capture(ring, a, prod)
             if events is not None:
                 events[i][1].record(prod)
+        if seal:  # as Observer.end_step: completes the step's last capture
+            ring.seal(prod)
 
     # roofline pass: one step of captures into an empty ring with the
     # staging engine idle, each launch bracketed by CUDA events on the
@@ -379,6 +381,7 @@ def leg_value(args, dist, dev):
                 torch.cuda.Event(enable_timing=True)) for _ in range(n_caps)]
     run_step(1, roof_ev)
     prod.synchronize()
+    ring.seal(prod)    # completion of the sealed captures (TF_CAP_SEALED)
     ring.note_launch(prod)
     roof_ms = [a.elapsed_time(b) for a, b in roof_ev]
     # the same step's launches back to back, one event pair around all of
@@ -391,6 +394,7 @@ def leg_value(args, dist, dev):
     run_step(2)
     span1.record(prod)
     prod.synchronize()
+    ring.seal(prod)    # completion of the sealed captures (TF_CAP_SEALED)
     ring.note_launch(prod)
     span_ms = span0.elapsed_time(span1)
     # and as a CUDA graph of the step's captures (how the model leg runs
@@ -401,13 +405,14 @@ def leg_value(args, dist, dev):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.stream(prod):
         with torch.cuda.graph(graph, stream=prod):
-            run_step(3)
+            run_step(3, seal=False)
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g0.record(prod)
     with torch.cuda.stream(prod):
         graph.replay()      # replays on the current stream
     g1.record(prod)
     prod.synchronize()
+    ring.seal(prod)    # completion of the sealed captures (TF_CAP_SEALED)
     ring.note_launch(prod)
     graph_span_ms = g0.elapsed_time(g1)
     del graph
@@ -430,6 +435,7 @@ def leg_value(args, dist, dev):
             gk.replay()
         k1.record(prod)
         prod.synchronize()
+        ring.seal(prod)    # completion of the sealed captures (TF_CAP_SEALED)
         ring.note_launch(prod)
         kind_us[label] = {"avg_launch_us": k0.elapsed_time(k1) * 1e3 / len(cap_args[kind::2]),
                           "bytes_per_launch": cap_args[kind][1]}
@@ -481,7 +487,10 @@ def leg_value(args, dist, dev):
         "d2h_seconds": stats1["transfer_seconds"] - stats0["transfer_seconds"],
         "stall_events": state.stall_events, "drops": state.drops,
         "clocks": clocks.summary(),
-        "launches": n_caps * args.steps * (1 if args.staging == "copy-engine" else 2),
+        # capture kernels (+ mapped-copy kernels when staging by SM stores)
+        # and one seal kernel per step
+        "launches": n_caps * args.steps * (1 if args.staging == "copy-engine" else 2)
+                    + args.steps,
     }
     pipe.close()
     ring.close()

@@ -80,6 +80,9 @@ typedef struct tf_descriptor {
  * handed out): the number of capture CTAs whose completion flags the host
  * must see before it may take the slot (0: posted after completion). */
 #define TF_DESC_CTA_SHIFT 16u
+/* Bit 15 of flags (device-internal, cleared before descriptors are handed
+ * out): posted by a TF_CAP_SEALED capture, complete per the rule above. */
+#define TF_DESC_PENDING 0x8000u
 
 typedef struct tf_ring_config {
   uint64_t payload_capacity; /* bytes, >0, multiple of 16 (rings.py:75-81) */
@@ -132,6 +135,13 @@ typedef struct tf_ring_state {
 #define TF_FULL_MASK 3u
 #define TF_CAP_DEFER_PUBLISH 0x4u  /* hooks.py:321-322: reserve + copy, no publish */
 #define TF_CAP_KEEP_PER_OUTER 0x8u /* keep[] indexed by outer index (request keep) */
+/* Completion by stream order (no reference analogue): the copy CTAs skip
+ * their fence and completion bytes; the descriptor is complete once a later
+ * capture on the same stream has posted the next descriptor, or a
+ * tf_ring_seal launched after it on that stream has run. Requires one
+ * producer stream per ring (as the producer snapshots do) and a seal at the
+ * end of every burst of captures (Observer.end_step / flush). */
+#define TF_CAP_SEALED 0x10u
 
 /* Element types. The first eight are DTYPE_WIDTHS (hooks.py:24-27); fp8
  * types are a north-star extension for cast captures. */
@@ -233,6 +243,9 @@ int tf_ring_release_payload(tf_ring* ring, uint64_t offset, uint64_t length);
 /* Wait until the device sees every release/poll made so far (the cursors
  * reach device memory through stream-ordered writes). */
 int tf_ring_sync_consumer(tf_ring* ring);
+/* Stream-ordered seal: once every earlier kernel on `stream` has completed,
+ * mark all descriptors posted so far complete (TF_CAP_SEALED captures). */
+int tf_ring_seal(tf_ring* ring, void* stream);
 /* Consumer-side totals the host already holds (no device access, no
  * synchronisation): reserved bytes released (dead skips excluded) and
  * descriptors consumed.

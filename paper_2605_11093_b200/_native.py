@@ -53,6 +53,8 @@ TF_FULL_RAISE = 0
 TF_FULL_WAIT = 1
 TF_FULL_DROP = 2
 TF_CAP_DEFER_PUBLISH = 0x4
+TF_CAP_SEALED = 0x10
+TF_DESC_PENDING = 0x8000
 TF_CAP_KEEP_PER_OUTER = 0x8
 
 TF_OP_COPY, TF_OP_CAST, TF_OP_REDUCE = 0, 1, 2
@@ -189,6 +191,7 @@ _SIGS = [
     ("tf_ring_poll_ready", C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(CDescriptor), u32p]),
     ("tf_ring_release_payload", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
     ("tf_ring_sync_consumer", C.c_int, [C.c_void_p]),
+    ("tf_ring_seal", C.c_int, [C.c_void_p, C.c_void_p]),
     ("tf_ring_get_state", C.c_int, [C.c_void_p, C.POINTER(CRingState)]),
     ("tf_ring_free_meta_slots", C.c_int, [C.c_void_p, u64p]),
     ("tf_ring_host_released", C.c_int, [C.c_void_p, u64p, u64p]),

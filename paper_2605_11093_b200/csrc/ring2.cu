@@ -347,6 +347,7 @@ struct CapParams {
   // launch-constant divisors (set_fastdiv); fd_ok: every dividend < 2^31
   FastDiv fd_spr, fd_rpu, fd_mid, fd_cg;
   uint32_t fd_ok;
+  uint64_t* seal;             // mapped host word: descriptors below it are complete
 };
 
 enum { MODE_COPY = 0, MODE_CAST = 1, MODE_REDUCE = 2 };
@@ -477,6 +478,13 @@ __device__ void leader_reserve(const CapParams& P, uint64_t bytes, uint64_t rows
         stalled = true;
         t0 = now;
         c->stall_events += 1;
+        // every earlier capture on this stream has finished (this grid is
+        // past griddepcontrol.wait): seal their descriptors, or a
+        // TF_CAP_SEALED predecessor would wait for a post this capture
+        // cannot make until the consumer frees its space
+        if (P.seal)
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.seal), "l"(c->meta_head)
+                       : "memory");
       } else if (now - t0 > P.timeout_ns) {
         c->stall_ns += now - t0;
         c->errors |= TF_DEVERR_TIMEOUT;
@@ -606,7 +614,7 @@ __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all
 // plan is known; the host takes the slot only when all n_ctas CTAs have set
 // their completion byte.
 __device__ void fast_desc(const CapParams& P, CapShared& sh, uint64_t bytes, uint64_t rows,
-                          uint32_t step, uint32_t n_ctas) {
+                          uint32_t step, uint32_t n_ctas, uint32_t pending) {
   tf_descriptor d;
   d.payload_offset = sh.off;
   d.payload_len = bytes;
@@ -614,7 +622,7 @@ __device__ void fast_desc(const CapParams& P, CapShared& sh, uint64_t bytes, uin
   d.step_seq = step;
   d.ready_seq = TF_READY_SENTINEL;
   d.skip_before = sh.fast_skip;
-  d.flags = sh.fast_kind | (n_ctas << TF_DESC_CTA_SHIFT);
+  d.flags = sh.fast_kind | (n_ctas << TF_DESC_CTA_SHIFT) | pending;
   d.n_rows = (uint32_t)rows;
   d.capture_seq = sh.fast_seq;
   d.checksum = 0;
@@ -986,8 +994,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
         sh.slot_idx = umod64(sh.fast_mh, P.slots);
       }
       // (every CTA builds it: whichever commits needs it; CTA 0 posts it)
-      if (!kCtl || blockIdx.x == 0 || !sh.flagmode)
-        fast_desc(P, sh, out_bytes, n_rows, step, sh.flagmode ? uint32_t(cg) : 0u);
+      if (!kCtl || blockIdx.x == 0 || !sh.flagmode) {
+        // sealed: completion follows from stream order (TF_CAP_SEALED), the
+        // copy CTAs report nothing
+        const bool sealed = sh.flagmode && (P.flags & TF_CAP_SEALED);
+        fast_desc(P, sh, out_bytes, n_rows, step,
+                  sh.flagmode && !sealed ? uint32_t(cg) : 0u, sealed ? TF_DESC_PENDING : 0u);
+      }
     } else {
       sh.flagmode = 0;
       uint32_t t = atomicAdd(&P.ctl->arrive, 1u);
@@ -1326,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     // once every byte is set). The controller committed the producer state
     // meanwhile. No last-CTA election, no round trip on the critical path.
     if (tid == 0) {
-      if (sh.publish && cb >= 0) {
+      if (sh.publish && cb >= 0 && !(P.flags & TF_CAP_SEALED)) {
 #if TF_FLAG_FENCE_SYS
         fence_acq_rel_sys();
 #else
@@ -1869,6 +1882,7 @@ static CapParams base_params(tf_ring* r) {
   P.dcons = r->dcons;
   P.ctl = r->ctl;
   P.done_flags = r->done_flags;
+  P.seal = r->seal_host;
   P.timeout_ns = r->cfg.wait_timeout_ns ? r->cfg.wait_timeout_ns : 30000000000ull;
   return P;
 }
@@ -1882,6 +1896,14 @@ static CapParams base_params(tf_ring* r) {
 __global__ void snapshot_kernel(const uint64_t* __restrict__ src, uint64_t* dst, int words) {
   for (int i = threadIdx.x; i < words; i += blockDim.x)
     dst[i] = ld_relaxed_gpu(src + i);
+}
+
+// Runs after every earlier kernel on its stream has completed (launched
+// without PDL): each descriptor below the committed meta head was posted by
+// a finished capture, so all of them are complete.
+__global__ void seal_kernel(const DevCtl* c, uint64_t* host_word) {
+  const uint64_t mh = *reinterpret_cast<const volatile uint64_t*>(&c->meta_head);
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(host_word), "l"(mh) : "memory");
 }
 
 static int snapshot(tf_ring* r) {
@@ -1919,6 +1941,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     if (r->meta) cudaFreeHost(r->meta);
     if (r->done_flags) cudaFreeHost(r->done_flags);
     if (r->ctl_host) cudaFreeHost(r->ctl_host);
+    if (r->seal_host) cudaFreeHost(r->seal_host);
     if (r->ctrl_stream) cudaStreamDestroy((cudaStream_t)r->ctrl_stream);
     delete r;
     return code;
@@ -1934,10 +1957,12 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
   if (cudaHostAlloc((void**)&r->meta, meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
       cudaHostAlloc((void**)&r->done_flags, size_t(cfg->meta_slots) * kMaxFlagCtas,
                     cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
-      cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+      cudaHostAlloc((void**)&r->ctl_host, sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&r->seal_host, 64, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
     tf_set_error("host arena allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(TF_ERR_ALLOCATION);
   }
+  memset(r->seal_host, 0, 64);
   memset(r->meta, 0, meta_bytes);
   memset(r->done_flags, 0, size_t(cfg->meta_slots) * kMaxFlagCtas);
   for (uint32_t s = 0; s < cfg->meta_slots; ++s)  // rings.py:213-215
@@ -1995,6 +2020,7 @@ extern "C" int tf_ring_destroy(tf_ring* r) {
   cudaFreeHost(r->meta);
   cudaFreeHost(r->done_flags);
   cudaFreeHost(r->ctl_host);
+  cudaFreeHost(r->seal_host);
   delete r;
   return TF_OK;
 }
@@ -2194,6 +2220,9 @@ extern "C" int tf_capture(tf_ring* r, void* stream, const tf_capture_args* a) {
   P.out_row_bytes = orb;
   P.keep_vec = ((uintptr_t)a->keep % 16) == 0;
   if ((a->flags & TF_FULL_MASK) > TF_FULL_DROP) { tf_set_error("bad full mode"); return TF_ERR_CONFIG; }
+  // a sealed capture is completed by the next descriptor: with one meta
+  // slot there is no next slot, so report per CTA instead
+  if (r->cfg.meta_slots < 2) P.flags &= ~TF_CAP_SEALED;
 
   // alignment every source row start shares (pow2, capped at 16)
   int sal = pow2_align((uintptr_t)a->src);
@@ -2469,6 +2498,20 @@ static bool slot_verified(const uint8_t* raw, tf_descriptor* d) {
 // The CTA count is stripped from the flags handed out.
 static bool slot_complete(const tf_ring* r, uint64_t slot, tf_descriptor* d) {
   if (!slot_verified(r->meta + slot * TF_DESCRIPTOR_SIZE, d)) return false;
+  if (d->flags & TF_DESC_PENDING) {
+    // TF_CAP_SEALED: complete once sealed, or once the next descriptor in
+    // sequence was posted by a later capture (which started only after this
+    // one finished: same stream, griddepcontrol.wait before its post)
+    bool done = __atomic_load_n(r->seal_host, __ATOMIC_ACQUIRE) > d->ready_seq;
+    if (!done) {
+      tf_descriptor nd;
+      const uint64_t ns = (slot + 1) % r->cfg.meta_slots;
+      done = ns != slot && slot_verified(r->meta + ns * TF_DESCRIPTOR_SIZE, &nd) &&
+             nd.ready_seq == d->ready_seq + 1 && !(nd.flags & TF_DESC_HOST_RESERVED);
+    }
+    if (!done) return false;
+    d->flags &= ~TF_DESC_PENDING;
+  }
   const uint32_t n = d->flags >> TF_DESC_CTA_SHIFT;
   if (n) {  // 8 completion bytes per load
     const uint8_t* f = r->done_flags + slot * kMaxFlagCtas;
@@ -2619,6 +2662,15 @@ extern "C" int tf_ring_host_released(tf_ring* r, uint64_t* bytes_released, uint6
   std::lock_guard<std::mutex> g(r->mu);
   if (bytes_released) *bytes_released = r->bytes_released;  // reservations, no dead skips
   if (consumed) *consumed = r->consumed;
+  return TF_OK;
+}
+
+extern "C" int tf_ring_seal(tf_ring* r, void* stream) {
+  if (!r) return TF_ERR_VALUE;
+  int rc = set_device(r->device);
+  if (rc) return rc;
+  seal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(r->ctl, r->seal_host);
+  CUDA_TRY(cudaGetLastError());
   return TF_OK;
 }
 

@@ -114,6 +114,7 @@ struct tf_ring {
   uint8_t* done_flags = nullptr;
   DevConsumer* dcons = nullptr;   // device
   DevCtl* ctl = nullptr;          // device
+  uint64_t* seal_host = nullptr;  // pinned, host-mapped: descriptors below it are complete
   DevCtl* ctl_host = nullptr;     // pinned, host-mapped snapshot target
   DevCtl* ctl_host_dev = nullptr; // its device alias (snapshot kernel)
   void* snap_stream = nullptr;    // high-priority stream of the snapshot kernel

@@ -78,7 +78,8 @@ class Observer:
                  sampled_hooks: frozenset = frozenset(),
                  rank_coords: tuple = (0, 0), wait_timeout: float = 60.0,
                  flat_rows: int = 0, persistent: bool = False,
-                 debug_row_bytes: dict | None = None, overlap: bool = False):
+                 debug_row_bytes: dict | None = None, overlap: bool = False,
+                 sealed: bool = True):
         t = torch()
         self.registry = registry
         self.policy = policy or PolicyConfig()
@@ -167,6 +168,10 @@ class Observer:
         self.overlap = overlap
         self.side_stream = t.cuda.Stream(device=dev) if overlap else None
         self._forked = False
+        # sealed=True: captures carry TF_CAP_SEALED (no per-CTA fence and
+        # completion bytes; completion follows from stream order) and
+        # end_step / flush / stop seal the ring on the producer stream
+        self.sealed = sealed
 
     # -- session -----------------------------------------------------------
 
@@ -176,6 +181,8 @@ class Observer:
         return self
 
     def stop(self, flush: bool = True) -> None:
+        self.join()
+        self._seal()
         if self.exporter.running:
             self.exporter.stop(flush=flush)
 
@@ -186,10 +193,15 @@ class Observer:
 
     def flush(self, timeout: float = 120.0) -> None:
         self.join()
+        self._seal()
         if self.side_stream is not None:
             self.side_stream.synchronize()  # every side-stream capture has published
         self.ring.sync()
         self.exporter.flush(timeout)
+
+    def _seal(self, stream=None) -> None:
+        if self.sealed:
+            self.ring.seal(stream)
 
     def join(self, stream=None) -> None:
         """Make the producer stream wait for the side-stream captures
@@ -405,6 +417,7 @@ class Observer:
 
     def end_step(self, stream=None) -> None:
         self.join(stream)
+        self._seal(stream)
         self.ring.note_launch(stream)
         self.active = self.persistent
 
@@ -479,7 +492,7 @@ class Observer:
         args = capture_args(
             src, hook_id=hook_id, hook=hook, keep_ptr=keep.data_ptr(),
             keep_per_outer=per_outer, step_seq_ptr=self.step_buf.data_ptr(),
-            full=self.policy.full_mode)
+            full=self.policy.full_mode, sealed=self.sealed)
         if self._need and not self._recording:
             q = self._need.get(hook.name)
             if q:
@@ -536,6 +549,10 @@ class Observer:
         rel = C.c_uint64()
         t0 = time.monotonic()
         rebased = False
+        # the last sealed capture completes only with a later post or a seal,
+        # and nothing is launched while the host waits here
+        self.join()
+        self._seal()
         while True:
             N.check(lib.tf_ring_host_released(self.ring.handle, C.byref(rel), None))
             self._released = rel.value

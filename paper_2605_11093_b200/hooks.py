@@ -373,7 +373,7 @@ def capture_args(src: RowSource, *, hook_id: int, hook: HookSpec | None = None,
                  keep_ptr: int = 0, keep_per_outer: bool = False,
                  step_seq: int = 0, step_seq_ptr: int = 0,
                  full: str = "wait", defer_publish: bool = False,
-                 max_ctas: int = 0) -> N.CCaptureArgs:
+                 max_ctas: int = 0, sealed: bool = False) -> N.CCaptureArgs:
     """Fill the C argument block for one capture launch."""
     if hook is not None:
         op = hook.op
@@ -384,6 +384,8 @@ def capture_args(src: RowSource, *, hook_id: int, hook: HookSpec | None = None,
     flags = FULL_MODES[full]
     if defer_publish:
         flags |= N.TF_CAP_DEFER_PUBLISH
+    if sealed:  # completion by stream order; the caller seals (RingPair.seal)
+        flags |= N.TF_CAP_SEALED
     if keep_per_outer:
         flags |= N.TF_CAP_KEEP_PER_OUTER
     return N.CCaptureArgs(

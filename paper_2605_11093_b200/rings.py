@@ -27,7 +27,7 @@ import struct
 from dataclasses import dataclass, field
 
 from . import _native as N
-from ._device import bytes_tensor, require_cuda, torch
+from ._device import bytes_tensor, require_cuda, stream_handle, torch
 from .errors import AllocationError, ConfigError
 
 COPY_UNIT = 16
@@ -273,6 +273,12 @@ class RingPair:
         ev, self._pending = self._pending, None
         if ev is not None:
             ev.synchronize()
+
+    def seal(self, stream=None) -> None:
+        """Stream-ordered: once the earlier work on `stream` (default: the
+        current stream) has run, every descriptor posted so far is complete
+        (captures launched with ``sealed=True``)."""
+        N.check(N.lib().tf_ring_seal(self.handle, stream_handle(stream, self.device)))
 
     def sync_consumer(self) -> None:
         """Wait until the device sees every release/poll made so far."""

@@ -30,6 +30,8 @@ ap.add_argument("--out", default="gpurun_out/sweep.json")
 ap.add_argument("--busy-d2h", action="store_true",
                 help="a 256 MiB pinned D2H loops on another stream during the timed "
                      "replays (PCIe saturated, as while the staging engine drains)")
+ap.add_argument("--sealed", action="store_true",
+                help="TF_CAP_SEALED captures (completion by stream order), one seal per replay")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -80,9 +82,15 @@ class BusyD2H:
         self.th.join()
 
 
+def seal():
+    if args.sealed:
+        ring.seal(s)
+
+
 def timed_graph(fn, reps):
     with torch.cuda.stream(s):
         fn()  # warm
+    seal()
     s.synchronize()
     drain()
     g = torch.cuda.CUDAGraph()
@@ -99,6 +107,7 @@ def timed_graph(fn, reps):
             e0.record()
             g.replay()
             e1.record()
+        seal()
         s.synchronize()
         if busy:
             busy.__exit__()
@@ -122,7 +131,7 @@ for nbytes in sizes:
         x = xs[i % len(xs)]
         src = RowSource(x.data_ptr(), B, mid, row, mid * row, row, x)
         caps.append(capture_args(src, hook_id=i, keep_ptr=keep.data_ptr(), keep_per_outer=True,
-                                 step_seq=0, full="wait"))
+                                 step_seq=0, full="wait", sealed=args.sealed))
 
     def cap_step():
         for a in caps:

@@ -13,9 +13,14 @@ nvcc $FL -Xcompiler -fsanitize=thread,-fPIC,-pthread,-g -ltsan -o /tmp/stress_ts
 N=${STRESS_N:-1500}
 ( time timeout 300 /tmp/stress_plain $N 1 ) > $O/plain_1ring.log 2>&1; echo "rc=$?" >> $O/plain_1ring.log
 ( time timeout 300 /tmp/stress_plain $N 2 ) > $O/plain_2rings.log 2>&1; echo "rc=$?" >> $O/plain_2rings.log
+( time timeout 300 /tmp/stress_plain $N 2 1 ) > $O/plain_2rings_sealed.log 2>&1; echo "rc=$?" >> $O/plain_2rings_sealed.log
 for tool in memcheck racecheck synccheck; do
   ( time timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 /tmp/stress_plain 300 1 ) > $O/cs_$tool.log 2>&1
   echo "rc=$?" >> $O/cs_$tool.log
+  ( time timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 /tmp/stress_plain 300 1 1 ) > $O/cs_${tool}_sealed.log 2>&1
+  echo "rc=$?" >> $O/cs_${tool}_sealed.log
 done
 ( time TSAN_OPTIONS="halt_on_error=0 second_deadlock_stack=1 report_signal_unsafe=0" timeout 900 /tmp/stress_tsan 600 2 ) > $O/tsan.log 2>&1
 echo "rc=$?" >> $O/tsan.log
+( time TSAN_OPTIONS="halt_on_error=0 second_deadlock_stack=1 report_signal_unsafe=0" timeout 900 /tmp/stress_tsan 600 2 1 ) > $O/tsan_sealed.log 2>&1
+echo "rc=$?" >> $O/tsan_sealed.log

@@ -151,6 +151,8 @@ static void consumer(Replica* R, uint64_t n_caps) {
   }
 }
 
+static bool g_sealed = false;  // argv[3]: TF_CAP_SEALED captures + seals
+
 static void producer(Replica* R, uint64_t n_caps) {
   for (uint64_t i = 0; i < n_caps; ++i) {
     const Shape s = shape_of(i);
@@ -170,16 +172,22 @@ static void producer(Replica* R, uint64_t n_caps) {
     a.step_seq = uint32_t(i);
     a.hook_id = uint32_t(i % 7);
     a.op = TF_OP_COPY;
-    a.flags = TF_FULL_WAIT | (s.per_outer ? TF_CAP_KEEP_PER_OUTER : 0u);
+    a.flags = TF_FULL_WAIT | (s.per_outer ? TF_CAP_KEEP_PER_OUTER : 0u) |
+              (g_sealed ? TF_CAP_SEALED : 0u);
     TK(tf_capture(R->ring, R->s, &a));
-    if (i % 64 == 63) CK(cudaStreamSynchronize(R->s));  // bound the fill backlog
+    if (i % 64 == 63) {  // bound the fill backlog
+      if (g_sealed) TK(tf_ring_seal(R->ring, R->s));
+      CK(cudaStreamSynchronize(R->s));
+    }
   }
+  if (g_sealed) TK(tf_ring_seal(R->ring, R->s));
   CK(cudaStreamSynchronize(R->s));
 }
 
 int main(int argc, char** argv) {
   const uint64_t n_caps = argc > 1 ? strtoull(argv[1], nullptr, 10) : 1500;
   const int n_rings = argc > 2 ? atoi(argv[2]) : 1;
+  g_sealed = argc > 3 && atoi(argv[3]) != 0;
   CK(cudaSetDevice(0));
   std::vector<Replica*> reps;
   for (int k = 0; k < n_rings; ++k) {

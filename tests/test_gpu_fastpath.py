@@ -37,7 +37,7 @@ class ListSink:
 
 
 def _stream(seed, n_caps, payload_capacity, meta_slots, host_every=0,
-            max_bytes=300_000):
+            max_bytes=300_000, sealed=False):
     rng = random.Random(seed)
     torch.manual_seed(seed)
     ring = RingPair(RingConfig(payload_capacity=payload_capacity, meta_slots=meta_slots))
@@ -55,6 +55,8 @@ def _stream(seed, n_caps, payload_capacity, meta_slots, host_every=0,
     for i in range(n_caps):
         if host_every and i % host_every == host_every - 1:
             # host protocol capture: reserve + write + publish on the host
+            if sealed:
+                ring.seal(s)
             s.synchronize()
             total = rng.randrange(16, 4096)
             need = round_up_to_copy_unit(total)
@@ -89,12 +91,14 @@ def _stream(seed, n_caps, payload_capacity, meta_slots, host_every=0,
         with torch.cuda.stream(s):
             launch_capture(ring, capture_args(src, hook_id=i, keep_ptr=kt.data_ptr(),
                                               keep_per_outer=True, step_seq=i,
-                                              full="wait"), s)
+                                              full="wait", sealed=sealed), s)
         launched += 1
         keepalive.append((x, kt))
         if len(keepalive) > 64:
             s.synchronize()
             keepalive.clear()
+    if sealed:
+        ring.seal(s)
     s.synchronize()
     pipe.stop(flush=True, timeout=120)
     got = [r.payload for r in sink.records]
@@ -186,3 +190,44 @@ def test_token_row_keep_up_to_256_rows(pattern):
         assert d.payload_len == len(want)
         assert bytes(ring.payload_view(d.payload_offset, d.payload_len)) == want, (rows, row)
         ring.close()
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_sealed_captures_complete_by_stream_order(seed):
+    """TF_CAP_SEALED: no per-CTA completion bytes; each descriptor completes
+    when the next capture on the stream posts, or at the seal. The ring
+    (1 MiB) is small enough that captures wait on the device, where the
+    waiting leader seals its predecessors."""
+    got, want, state, counters, _ = _stream(seed, 300, 1 << 20, 16, sealed=True)
+    assert len(got) == len(want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g == w, f"record {i} differs"
+    assert state.occupancy == 0 and counters["drops"] == 0
+
+
+def test_sealed_with_host_protocol_and_tiny_meta_ring():
+    got, want, state, counters, _ = _stream(23, 200, 1 << 20, 2, host_every=7,
+                                            max_bytes=20_000, sealed=True)
+    assert got == want
+    assert state.occupancy == 0 and counters["drops"] == 0
+
+
+def test_sealed_last_capture_waits_for_the_seal():
+    """The newest sealed descriptor is not handed out until a seal (or a
+    later capture) completes it."""
+    ring = RingPair(RingConfig(payload_capacity=1 << 20, meta_slots=16))
+    s = torch.cuda.Stream()
+    x = torch.randint(0, 256, (4, 1, 4096), dtype=torch.uint8, device="cuda")
+    kt = torch.ones(4, dtype=torch.uint8, device="cuda")
+    src = RowSource(x.data_ptr(), 4, 1, 4096, 4096, 4096, x)
+    with torch.cuda.stream(s):
+        for i in range(3):
+            launch_capture(ring, capture_args(src, hook_id=i, keep_ptr=kt.data_ptr(),
+                                              keep_per_outer=True, step_seq=i,
+                                              full="wait", sealed=True), s)
+    s.synchronize()
+    assert ring.ready_entries() == 2      # the third waits for its seal
+    ring.seal(s)
+    s.synchronize()
+    assert ring.ready_entries() == 3
+    ring.close()
