@@ -4,7 +4,7 @@ O=gpurun_out/s3seal; mkdir -p $O
 ( time timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider ) > $O/pytest.log 2>&1
 for sl in "" "--sealed"; do
   for busy in "" "--busy-d2h"; do
-    tag=${sl:+sealed}${sl:-flags}${busy:+_busy}
+    tag=$([ -n "$sl" ] && echo sealed || echo flags)${busy:+_busy}
     timeout 300 python scripts/exp_sweep.py --n 32 --batch 16 --sizes-kb 128,448 --row-bytes 8192 $sl $busy --reps 7 --out $O/dec_$tag.json > $O/dec_$tag.log 2>&1
     timeout 300 python scripts/exp_sweep.py --n 16 --sizes-kb 1024,32768,114688 --row-bytes 8192 $sl $busy --reps 7 --out $O/big_$tag.json > $O/big_$tag.log 2>&1
   done
