@@ -907,31 +907,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
     }
   }
 
-  // REDUCE on 8-element groups: this warp's first row and its first batch
-  // of loads, speculatively under the identity row map (as the copy path),
-  // so the reads overlap the keep scan and the plan
-  constexpr int kRNR = IN_DT == TF_F32 ? 2 : 1;
-  constexpr int kRRU = IN_DT == TF_F32 ? kUnroll / 2 : kUnroll;
-  uint4 rspec[(MODE == MODE_REDUCE && VW == 8) ? kRRU : 1][kRNR];
-  int64_t rspec_row = -1;
-  if constexpr (MODE == MODE_REDUCE && VW == 8) {
-    const int64_t j0 = int64_t(cb) * kWarps + warp;
-    if (cb >= 0 && (!P.keep || U <= kThreads) && j0 < U * P.rpu) {
-      const uint8_t* src = row_src(P, j0);
-      const int64_t G8 = P.row_elems / 8;
-      constexpr int WI = Elem<IN_DT>::W;
-#pragma unroll
-      for (int u = 0; u < kRRU; ++u) {
-        const int64_t g = lane + int64_t(u) * 32;
-        if (g < G8) {
-#pragma unroll
-          for (int q = 0; q < kRNR; ++q) rspec[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
-        }
-      }
-      rspec_row = j0;
-    }
-  }
-
   // ---- 1. ordered compaction: count kept units (batch order, no atomics) ----
   // Each thread owns a run of whole 16-unit groups; the first group stays
   // in registers for the rank table below (one keep load per thread in the
@@ -1290,25 +1265,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
           float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
           if (VW == 8) {
             const int64_t G8 = H / 8;
-            constexpr int NR = kRNR;
-            constexpr int RU = kRRU;  // loads in flight
-            // the speculative batch holds iff the kept rows are a prefix
-            const bool spec_ok = j == rspec_row && prefix;
+            constexpr int NR = IN_DT == TF_F32 ? 2 : 1;
+            constexpr int RU = IN_DT == TF_F32 ? kUnroll / 2 : kUnroll;  // loads in flight
             for (int64_t g0 = lane; g0 < G8; g0 += 32 * RU) {
               uint4 raw[RU][NR];
-              if (spec_ok && g0 == lane) {
 #pragma unroll
-                for (int u = 0; u < RU; ++u)
+              for (int u = 0; u < RU; ++u) {
+                const int64_t g = g0 + int64_t(u) * 32;
+                if (g < G8) {
 #pragma unroll
-                  for (int q = 0; q < NR; ++q) raw[u][q] = rspec[u][q];
-              } else {
-#pragma unroll
-                for (int u = 0; u < RU; ++u) {
-                  const int64_t g = g0 + int64_t(u) * 32;
-                  if (g < G8) {
-#pragma unroll
-                    for (int q = 0; q < NR; ++q) raw[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
-                  }
+                  for (int q = 0; q < NR; ++q) raw[u][q] = ld_stream<16>(src + g * 8 * WI + 16 * q);
                 }
               }
 #pragma unroll
