@@ -77,6 +77,8 @@ def build(force: bool = False, verbose: bool = False,
                 defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")
             elif part.startswith("u"):
                 defines.append(f"-DTF_UNROLL={int(part[1:])}")
+            elif part == "nostcs":  # plain (evict-normal) ring stores (A/B)
+                defines.append("-DTF_ST_CS=0")
             elif part == "nospec0":
                 defines.append("-DTF_SPEC_WARP0=0")
             elif part.startswith("smem"):  # trace_smemN: N shared-memory spec segments
