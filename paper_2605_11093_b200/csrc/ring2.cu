@@ -857,7 +857,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // one byte per thread, ranks by warp ballots, the whole rank table in
   // shared memory
   const bool small = P.keep && U <= kThreads;
-  const uint32_t kbyte = (small && tid < U) ? P.keep[tid] : 0u;
+  // <= 32 keep units (a request keep, or the token rows of a small decode
+  // step): every warp loads the same 32 keep bytes and ranks them with its
+  // own ballot, so no block barrier is needed before the plan
+  const bool tiny = small && U <= 32;
+  const int kidx = tiny ? lane : tid;
+  const uint32_t kbyte = (small && kidx < U) ? P.keep[kidx] : 0u;
   // COPY: speculatively load this warp's first segment of the
   // grid-interleaved order assuming every unit is kept (identity row map),
   // so the source read overlaps the keep/snapshot round trip; used only if
@@ -931,7 +936,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) capture_kernel(CapParams
   // <= 32 keep units (request keep): one warp, one coalesced load, ranks by
   // ballot; the whole rank table is built here and indexed from rank 0
   bool prefix = !P.keep;  // kept units are exactly units [0, K): identity map
-  if (small) {
+  if (tiny) {
+    const uint32_t m = __ballot_sync(0xffffffffu, kbyte != 0);
+    const uint32_t tot = __popc(m);
+    if (warp == 0 && kbyte) sh.table[__popc(m & ((1u << lane) - 1u))] = uint32_t(lane);
+    K = tot;
+    prefix = m == (tot == 32 ? 0xffffffffu : (1u << tot) - 1u);  // kept units are [0, K)
+    TSTAMP(t_scan);
+  } else if (small) {
     const uint32_t m = __ballot_sync(0xffffffffu, kbyte != 0);
     if (lane == 0) sh.warp_sums[warp] = __popc(m);
     __syncthreads();
