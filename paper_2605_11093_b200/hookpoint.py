@@ -200,7 +200,7 @@ class Observer:
         self.exporter.flush(timeout)
 
     def _seal(self, stream=None) -> None:
-        if self.sealed:
+        if self.sealed and getattr(self.ring, "_h", None) is not None:
             self.ring.seal(stream)
 
     def join(self, stream=None) -> None:
