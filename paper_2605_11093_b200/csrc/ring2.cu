@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1892,6 +1893,55 @@ __global__ void publish_kernel(CapParams P, tf_descriptor d) {
 // ---------------------------------------------------------------------------
 // host: ring lifecycle
 // ---------------------------------------------------------------------------
+// CUDA loads kernels lazily (CUDA_MODULE_LOADING=LAZY by default): the first
+// launch of a kernel loads it, and loading can wait on the device. A first
+// launch made while a capture kernel waits on the device for the staging
+// engine (the seal at the end of the first step, a snapshot) then deadlocks
+// with it. So every kernel this library can launch is loaded when the first
+// ring is created (querying a kernel's attributes loads it).
+template <int MODE, int VW, int IN, int OUT, int SS = kSmemSpec>
+static void touch() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, capture_kernel<MODE, VW, IN, OUT, SS>);
+}
+template <int IN, int OUT>
+static void touch_cast() {
+  touch<MODE_CAST, 8, IN, OUT>();
+  touch<MODE_CAST, 1, IN, OUT>();
+}
+template <int IN>
+static void touch_in() {
+  touch_cast<IN, TF_F32>();
+  touch_cast<IN, TF_F16>();
+  touch_cast<IN, TF_BF16>();
+  touch_cast<IN, TF_F8E4M3>();
+  touch_cast<IN, TF_F8E5M2>();
+  touch<MODE_REDUCE, 8, IN, TF_F32>();
+  touch<MODE_REDUCE, 1, IN, TF_F32>();
+}
+__global__ void seal_kernel(const DevCtl* c, uint64_t* host_word);
+__global__ void snapshot_kernel(const uint64_t* __restrict__ src, uint64_t* dst, int words);
+static void preload_kernels() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    touch<MODE_COPY, 16, 0, 0>();
+    touch<MODE_COPY, 16, 0, 0, 0>();
+    touch<MODE_COPY, 8, 0, 0>();
+    touch<MODE_COPY, 4, 0, 0>();
+    touch<MODE_COPY, 2, 0, 0>();
+    touch<MODE_COPY, 1, 0, 0>();
+    touch_in<TF_F32>();
+    touch_in<TF_F16>();
+    touch_in<TF_BF16>();
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, seal_kernel);
+    cudaFuncGetAttributes(&a, snapshot_kernel);
+    cudaFuncGetAttributes(&a, reserve_kernel);
+    cudaFuncGetAttributes(&a, publish_kernel);
+    cudaGetLastError();
+  });
+}
+
 static int set_device(int dev) {
   CUDA_TRY(cudaSetDevice(dev));
   return TF_OK;
@@ -2021,6 +2071,7 @@ extern "C" int tf_ring_create(const tf_ring_config* cfg, int device, tf_ring** o
     return fail(TF_ERR_CUDA);
   }
   r->snap_stream = s;
+  preload_kernels();
   if (kSmemSpec > 0 && kSpecSmemBytes > 48 * 1024 &&
       cudaFuncSetAttribute(capture_kernel<MODE_COPY, 16, 0, 0>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -334,6 +334,11 @@ extern "C" int tf_stager_create(tf_ring* ring, const tf_drain_config* cfg, tf_st
     return TF_ERR_CUDA;
   }
   cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, st->device);
+  {  // load the staging kernel now, not lazily at its first launch (ring2.cu preload_kernels)
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, mapped_copy_kernel);
+    cudaGetLastError();
+  }
   st->cpus = gpu_local_cpus(st->device);
   if (cfg->numa_node == -2) st->cpus.clear();  // explicit opt-out
   // allocate the pinned pool from a thread bound near the GPU (first touch)
