@@ -256,9 +256,9 @@ class Observer:
                 fe = plan.fifo_entries
                 lens = fe.payload_lens() if isinstance(fe, StepMetas) else \
                     [m.expected_payload_len for m in fe]
-                for n in lens:
-                    since += n + 16
-                    big = max(big, n)
+                if lens:
+                    since += sum(lens) + 16 * len(lens)
+                    big = max(big, max(lens))
                 self._sc = (st, t0, since, big)
         if plan.flush_before:
             self.flush()
@@ -416,6 +416,8 @@ class Observer:
         return self._batch[0].token_start if self._batch else 0
 
     def end_step(self, stream=None) -> None:
+        if stream is None:  # resolved once (a torch call costs microseconds)
+            stream = torch().cuda.current_stream(self.device)
         self.join(stream)
         self._seal(stream)
         self.ring.note_launch(stream)

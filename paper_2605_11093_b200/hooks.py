@@ -210,6 +210,30 @@ class HookRegistry:
             c[tokens] = e
         return e
 
+    def step_entries(self, tokens: int, ragged: bool) -> tuple:
+        """The planner's per-step view of plan_entries, cached the same way:
+        (entries, per) with entries = [(name, layer, shape, out_dtype)] in
+        firing order and per the record bytes of each per token row
+        (ragged) or per request (uniform), so a step's payload lengths are
+        rows x per, or requests x per.
+        ragged=True validates once that every hook leads with tokens."""
+        key = ("step", tokens, ragged)
+        c = self._plan_cache
+        e = c.get(key) if c.get(None) is self._enabled else None
+        if e is None:
+            entries = []
+            per = []
+            for hid, hook, shape in self.plan_entries(tokens):
+                if ragged and (hook.dims[0] != "tokens" or "tokens" in hook.dims[1:]):
+                    raise ConfigError(
+                        f"ragged capture needs hook {hook.name!r} to lead with tokens")
+                entries.append((hook.name, hook.layer_index, shape, hook.out_dtype))
+                # ragged: bytes per token row; uniform: bytes per request
+                per.append(math.prod(shape[1:] if ragged else shape) * hook.out_dtype.width)
+            e = (tuple(entries), tuple(per))
+            c[key] = e   # (plan_entries above has reset the cache if the set changed)
+        return e
+
 
 def install_hooks(model: ModelSpec, specs: list[HookSpec],
                   layers: list[int] | None = None,
