@@ -79,6 +79,7 @@ class Observer:
                  rank_coords: tuple = (0, 0), wait_timeout: float = 60.0,
                  flat_rows: int = 0, persistent: bool = False,
                  debug_row_bytes: dict | None = None, overlap: bool = False,
+                 overlap_max_bytes: int | None = None,
                  sealed: bool = True):
         t = torch()
         self.registry = registry
@@ -166,6 +167,10 @@ class Observer:
         # the captures stay serialised among themselves, as the producer
         # snapshot protocol requires.
         self.overlap = overlap
+        # overlap_max_bytes: fork only captures whose source is at most this
+        # large (decode-size captures overlap well; large ones compete with
+        # the model for SMs); larger ones run inline after a join
+        self.overlap_max_bytes = overlap_max_bytes
         self.side_stream = t.cuda.Stream(device=dev) if overlap else None
         self._forked = False
         # sealed=True: captures carry TF_CAP_SEALED (no per-CTA fence and
@@ -499,7 +504,13 @@ class Observer:
             q = self._need.get(hook.name)
             if q:
                 self._admit(q.pop())
-        if self.overlap:
+        fork = self.overlap and (self.overlap_max_bytes is None or
+                                 src.outer * src.mid * src.row_bytes <= self.overlap_max_bytes)
+        if self.overlap and not fork:
+            # inline after the forked ones: captures stay serialised on the
+            # ring (one producer order for snapshots and sealed completion)
+            self.join(stream)
+        if fork:
             t = torch()
             cur = stream if stream is not None else t.cuda.current_stream(self.device)
             side = self.side_stream

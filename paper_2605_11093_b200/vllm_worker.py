@@ -226,7 +226,8 @@ class ObservedWorker(Worker):
                               split_oversize=True),
             policy=policy, sink=self._tf_sink, device=self.local_rank,
             max_batch=max_seqs, flat_rows=max_tokens + 1024, persistent=True,
-            debug_row_bytes=dbg_rows, overlap=bool(cfg.get("overlap", False)))
+            debug_row_bytes=dbg_rows, overlap=bool(cfg.get("overlap", False)),
+            overlap_max_bytes=cfg.get("overlap_max_bytes"))
         # records that outlive the batch (ListSink) must own their bytes
         obs.exporter.copy_payloads = cfg.get("sink") == "list"
         obs.start()

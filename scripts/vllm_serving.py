@@ -40,6 +40,8 @@ ap.add_argument("--gpu-mem", type=float, default=0.55)
 ap.add_argument("--ring-gib", type=float, default=8.0)
 ap.add_argument("--overlap", action="store_true",
                 help="capture kernels on the observer's side stream (overlap mode)")
+ap.add_argument("--overlap-max-kib", type=int, default=0,
+                help="overlap mode: fork only captures up to this size (0 = all)")
 args = ap.parse_args()
 
 d = tempfile.mkdtemp(prefix="llama3_8b_")
@@ -56,7 +58,8 @@ if args.capture == "on":
     os.environ["TF_VLLM_OBSERVER"] = json.dumps({
         "sites": args.sites.split(","), "ring_bytes": int(args.ring_gib * (1 << 30)),
         "meta_slots": 8192, "policy": args.policy, "sink": "null",
-        "overlap": args.overlap})
+        "overlap": args.overlap,
+        "overlap_max_bytes": (args.overlap_max_kib << 10) or None})
     kw["worker_cls"] = "paper_2605_11093_b200.vllm_worker.ObservedWorker"
 
 from vllm import LLM, SamplingParams  # noqa: E402
@@ -114,7 +117,7 @@ def serve(rate):
     ttft = [(first[r] - arrivals[r]) * 1e3 for r in first]
     line = {"config": "llama3-8b-vllm-online", "capture": args.capture,
             "sites": args.sites if args.capture == "on" else None, "policy": args.policy,
-            "overlap": args.overlap,
+            "overlap": args.overlap, "overlap_max_kib": args.overlap_max_kib,
             "rate_rps": rate, "requests": args.num_requests,
             "prompt_len": args.prompt_len, "output_len": args.output_len,
             "tpot_ms_mean": statistics.mean(tpot), "tpot_ms_median": statistics.median(tpot),

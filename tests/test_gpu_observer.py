@@ -540,3 +540,53 @@ def test_overlap_side_stream_captures_before_in_place_update(graph):
     obs.close()
     got = [(r.request_id, r.hook_name, r.step_seq, bytes(r.payload)) for r in sink.records]
     assert sorted(got) == sorted(expected)
+
+
+def test_overlap_threshold_mixes_forked_and_inline_captures():
+    """overlap_max_bytes: small captures fork onto the side stream, large
+    ones run inline after a join; inside one recorded graph the two kinds
+    alternate and every record stays byte-exact (the ring sees one order)."""
+    B, T, H, h, L = 4, 32, 512, 32, 3
+    reg = install_hooks(ModelSpec(L, H), [
+        HookSpec("big", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+        HookSpec("small", ("tokens", h), DType.of("bf16"), per_layer=True)])
+    sink = Collect()
+    obs = Observer(reg, ring=RingConfig(16 << 20, 256), sink=sink, max_batch=B,
+                   drain=DrainConfig(min_ready_entries=1), overlap=True,
+                   overlap_max_bytes=B * T * h * 2)
+    obs.start()
+    x = torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda")
+    bigs = [torch.zeros(B, T, H, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+    smalls = [torch.zeros(B, T, h, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+
+    def body():
+        for i in range(L):
+            bigs[i].copy_(x * (i + 1))
+            smalls[i].copy_(x[..., :h] - i)
+            obs.capture(obs.hook_id(f"big[{i}]"), bigs[i])
+            obs.capture(obs.hook_id(f"small[{i}]"), smalls[i])
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        body()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with obs.graph_capture(), torch.cuda.graph(g):
+        body()
+    expected = []
+    for step in range(3):
+        x.copy_(torch.randn(B, T, H, dtype=torch.bfloat16))
+        obs.begin_step([StepRequest(i, i, "p", T, 0) for i in range(B)], 30 + step)
+        g.replay()
+        obs.end_step()
+        torch.cuda.synchronize()
+        for i in range(L):
+            for b in range(B):
+                for name, t in ((f"big[{i}]", bigs[i]), (f"small[{i}]", smalls[i])):
+                    expected.append((b, name, 30 + step,
+                                     t[b].contiguous().view(torch.uint8).cpu().numpy().tobytes()))
+    obs.flush()
+    obs.close()
+    got = [(r.request_id, r.hook_name, r.step_seq, bytes(r.payload)) for r in sink.records]
+    assert sorted(got) == sorted(expected)
