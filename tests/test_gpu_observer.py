@@ -565,6 +565,7 @@ def test_overlap_threshold_mixes_forked_and_inline_captures():
             smalls[i].copy_(x[..., :h] - i)
             obs.capture(obs.hook_id(f"big[{i}]"), bigs[i])
             obs.capture(obs.hook_id(f"small[{i}]"), smalls[i])
+        obs.join()   # forked work must rejoin before a graph recording ends
 
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
