@@ -345,3 +345,35 @@ def test_step_metas_fifo_materialises_lazily_in_order():
     for m in sm:
         assert fifo.match(d(m.hook_name, m.expected_payload_len), m.hook_name) == m
     assert len(fifo) == 0 and fifo.peek() is None
+
+
+def test_step_entries_payload_lens_match_the_uncached_formula():
+    """HookRegistry.step_entries caches per-entry byte factors; StepMetas
+    payload lengths built from them equal the per-entry shape formula for
+    uniform batches (per request) and ragged ones (per token row)."""
+    from paper_2605_11093_b200.hooks import DType, HookSpec, ModelSpec, install_hooks
+    from paper_2605_11093_b200.records import StepMetas, TensorMeta
+    reg = install_hooks(ModelSpec(2, 64), [
+        HookSpec("resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+        HookSpec("attn", (4, "tokens", "tokens"), DType.of("f32"), per_layer=True),
+        HookSpec("red", ("tokens", "hidden"), DType.of("bf16"), per_layer=True,
+                 reduce="stats")])
+    entries, per = reg.step_entries(5, False)
+    name, layer, shape, dt = entries[0]
+    base = TensorMeta(name, layer, 3, (1, 2, 3), ((0, 5),) * 3, shape, dt)
+    assert StepMetas(base, entries, per).payload_lens() == \
+        StepMetas(base, list(entries)).payload_lens()
+    reg2 = install_hooks(ModelSpec(2, 64), [
+        HookSpec("resid", ("tokens", "hidden"), DType.of("bf16"), per_layer=True),
+        HookSpec("mlp", ("tokens", 128), DType.of("bf16"), per_layer=True)])
+    entries, per = reg2.step_entries(7, True)
+    name, layer, shape, dt = entries[0]
+    base = TensorMeta(name, layer, 3, (1, 2), ((0, 3), (0, 7)), shape, dt,
+                      row_counts=(3, 7))
+    assert StepMetas(base, entries, per).payload_lens() == \
+        StepMetas(base, list(entries)).payload_lens()
+    # the ragged view rejects a hook whose tokens axis is not first
+    import pytest as _pt
+    from paper_2605_11093_b200.errors import ConfigError
+    with _pt.raises(ConfigError):
+        reg.step_entries(5, True)
