@@ -77,6 +77,8 @@ def build(force: bool = False, verbose: bool = False,
                 defines.append(f"-DTF_CTAS_PER_SM={int(part[1:])}")
             elif part.startswith("u"):
                 defines.append(f"-DTF_UNROLL={int(part[1:])}")
+            elif part == "nopreload":  # lazy kernel loading (repro of the hang)
+                defines.append("-DTF_NO_PRELOAD")
             elif part == "nostcs":  # plain (evict-normal) ring stores (A/B)
                 defines.append("-DTF_ST_CS=0")
             elif part == "nospec0":
